@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""PARS3 benchmark: skew-symmetric SpMV GB/s (fraction of HBM roofline) and GFLOP/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl pars3|reference]
+
+Workload (default): BASELINE.json config c5, A = 0.5*I + S with S the 3-D
+27-point stencil graph on a 256^3 grid (n = 16,777,216, m = 216,338,940
+stored lower entries), RCM-reordered and split at the reference's default
+beta -- the largest single-GPU configuration, on which the north star's 70%
+target is quoted.  One step = one MRS-style iteration: y = A x fused with
+the inner product <y, y>.  Preprocessing (generation, RCM, split, plan,
+upload) is outside the clock, as in the reference (bench.py:1-8 of the
+reference).
+
+Bytes per SpMV are the algorithmic count of SURVEY.md 8(d):
+    B = 12 m + 4 (n + 1) + 24 n
+(fp64 value + int32 column per stored entry, int32 row pointer, diagonal,
+x read, y write); flops F = 4 m + 2 n (count_ops, serial.py:28-47).
+The matrix stream (3.07 GB) is far larger than the 126 MB L2, so no L2
+flush is needed between steps.
+
+--impl reference times the reference algorithm on the host cores instead:
+the C restatement of the reference's _pars3 kernel (oracle/oracle.c,
+OpenMP, p = all host cores), the reference package itself being a numba
+library that is not shipped to the GPU box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "skew-SpMV GB/s (frac of HBM roofline) and GFLOP/s, fp64, at 1/2/4/8 B200"
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def algorithmic_bytes(n: int, m: int) -> int:
+    return 12 * m + 4 * (n + 1) + 24 * n
+
+
+def algorithmic_flops(n: int, m: int) -> int:
+    return 4 * m + 2 * n
+
+
+def peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def build_problem(cfg: str, beta=None):
+    """Generator -> pattern -> RCM -> relabel -> split (native pipeline)."""
+    import numpy as np
+
+    import paper_2407_17651_b200 as P
+    from paper_2407_17651_b200 import generators as G
+    t0 = time.time()
+    g = G.make_config(cfg)
+    t1 = time.time()
+    m0 = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
+    del g
+    perm = P.rcm_order(P.pattern_from_sss(m0))
+    t2 = time.time()
+    m = P.permute_sss(m0, perm)
+    del m0
+    bw = P.compute_bandwidth(m)
+    if beta is None:
+        beta = P.default_beta(m.n, bw)
+    s = P.split_bands(m, beta)
+    t3 = time.time()
+    x = G.make_x(m.n, G.CONFIGS[cfg]["seed_x"])
+    log(f"{cfg}: n={m.n} m={m.nnz_offdiag} rcm_bw={bw} beta={beta} mid={s.middle_count} "
+        f"outer={s.outer_count}; gen {t1 - t0:.1f}s rcm {t2 - t1:.1f}s permute+split {t3 - t2:.1f}s")
+    return m, s, bw, beta, np.ascontiguousarray(x)
+
+
+class ClockSampler:
+    """nvidia-smi sampled every 100 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(s, x, n, m, reps_max=10, min_seconds=10.0):
+    """The reference algorithm (C restatement of _pars3, parallel.py:60-120)
+    on all host cores, p = cores: bounded sample of the same workload."""
+    import numpy as np
+
+    from oracle import oracle as O
+    cores = len(os.sched_getaffinity(0))
+    O.build()
+    split = {"n": s.n, "beta": s.beta, "mid_ptr": s.mid_ptr, "mid_col": s.mid_col.astype(np.int64),
+             "mid_val": s.mid_val, "diag": s.diag, "outer_row": s.outer_row.astype(np.int64),
+             "outer_col": s.outer_col.astype(np.int64), "outer_val": s.outer_val}
+    plan = O.classify_conflicts(split, O.partition_rows(s.n, cores))
+    O.spmv_pars3(split, plan, x, nthreads=cores)  # warm-up
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < reps_max and (time.perf_counter() - t_all) < min_seconds or len(times) < 3:
+        t0 = time.perf_counter()
+        O.spmv_pars3(split, plan, x, nthreads=cores)
+        times.append(time.perf_counter() - t0)
+    mean = sum(times) / len(times)
+    return {"value": algorithmic_bytes(n, m) / mean / 1e9, "unit": "GB/s", "cores": cores,
+            "kind": "port", "sample": f"{len(times)} full SpMVs (oracle C _pars3 restatement, "
+            f"p={cores}, OpenMP {cores} threads), mean {mean * 1e3:.1f} ms",
+            "gflops": algorithmic_flops(n, m) / mean / 1e9, "ms_per_spmv": mean * 1e3}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host cores (rank 0)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    m, s, bw, beta, x = build_problem(args.config, args.beta)
+    import numpy as np
+
+    from oracle import oracle as O
+    cores = len(os.sched_getaffinity(0))
+    O.build()
+    split = {"n": s.n, "beta": s.beta, "mid_ptr": s.mid_ptr, "mid_col": s.mid_col.astype(np.int64),
+             "mid_val": s.mid_val, "diag": s.diag, "outer_row": s.outer_row.astype(np.int64),
+             "outer_col": s.outer_col.astype(np.int64), "outer_val": s.outer_val}
+    plan = O.classify_conflicts(split, O.partition_rows(s.n, cores))
+    for _ in range(args.warmup):
+        O.spmv_pars3(split, plan, x, nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        y = O.spmv_pars3(split, plan, x, nthreads=cores)
+        float(y @ y)  # the step's inner product
+    dt = (time.perf_counter() - t0) / args.steps
+    n, nnz = m.n, m.nnz_offdiag
+    val = algorithmic_bytes(n, nnz) / dt / 1e9
+    out = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, BASELINE config)",
+        "config": {"workload": args.config, "n": n, "nnz_lower": nnz, "beta": beta,
+                   "rcm_bandwidth": bw, "p": cores},
+        "gflops": algorithmic_flops(n, nnz) / dt / 1e9,
+        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full SpMV + dot steps (oracle C _pars3 "
+                                   f"restatement, p={cores})"},
+        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    import paper_2407_17651_b200 as P
+    from oracle import oracle as O
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    m, s, bw, beta, x_host = build_problem(args.config, args.beta)
+    n, nnz = m.n, m.nnz_offdiag
+    plan, _ = P.classify_conflicts(s, P.partition_rows(n, 1))
+    t0 = time.time()
+    op = P.prepare(s, plan)
+    torch.cuda.synchronize()
+    log(f"upload + device plan {time.time() - t0:.1f}s, plan bytes {op.plan_bytes()}")
+    x = torch.from_numpy(x_host).cuda()
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    dot = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    # parity check of this run's product against the oracle (outside the clock)
+    op.matvec(x, y)
+    torch.cuda.synchronize()
+    y_ref = O.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x_host) \
+        if rank == 0 and not args.no_check else None
+    parity = O.rel_err(y.cpu().numpy(), y_ref) if y_ref is not None else None
+    log(f"parity rel_err vs oracle serial: {parity}")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    for _ in range(args.warmup):
+        op.matvec_dot(x, y, y, dot)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            op.matvec_dot(x, y, y, dot)
+        ev1.record()
+        barrier()
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    if dist is not None:
+        t = torch.tensor([step_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = float(t.item())
+
+    # dominant kernel: the SpMV alone, same clock discipline
+    barrier()
+    ev0.record()
+    for _ in range(args.steps):
+        op.matvec(x, y)
+    ev1.record()
+    barrier()
+    spmv_ms = ev0.elapsed_time(ev1) / args.steps
+
+    # end to end through the public API: pinned host x in, host y out
+    x_pin = torch.from_numpy(x_host).pin_memory()
+    y_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+    P.spmv_pars3(s, plan, x_pin, out=y_pin)
+    barrier()
+    t_e = time.perf_counter()
+    ev0.record()
+    for _ in range(args.steps):
+        P.spmv_pars3(s, plan, x_pin, out=y_pin)
+    ev1.record()
+    barrier()
+    e2e_ms = ev0.elapsed_time(ev1) / args.steps
+    e2e_wall_ms = (time.perf_counter() - t_e) * 1e3 / args.steps
+
+    B = algorithmic_bytes(n, nnz)
+    F = algorithmic_flops(n, nnz)
+    peak, peak_src = peak_hbm()
+    value = world * B / (step_ms * 1e-3) / 1e9
+    achieved = B / (spmv_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config)
+        except Exception:
+            traffic = None
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(s, x_host, n, nnz)
+    out = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, BASELINE config; random-init values U(-1,1))",
+        "config": {"workload": args.config, "n": n, "nnz_lower": nnz, "beta": beta,
+                   "rcm_bandwidth": bw, "step": "y = A x fused with <y, y>",
+                   "bytes_per_spmv": B, "flops_per_spmv": F,
+                   "l2": "inputs larger than L2 (matrix stream 3.07 GB per step)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "gflops": world * F / (step_ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel_ms": spmv_ms, "frac_of_8TBs": achieved / 8000.0},
+        "cpu_baseline": cpu,
+        "e2e": {"value": B / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms, "wall_ms_per_step": e2e_wall_ms,
+                "api": "spmv_pars3(s, plan, x_pinned_host_tensor, out=y_pinned_host_tensor)"},
+        "gpu_launches": args.steps * op.kernel_count(with_dot=True),
+        "clocks": clk.summary(),
+        "parity_rel_err": parity,
+    }
+    print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--beta", type=int, default=None)
+    ap.add_argument("--impl", default="pars3", choices=["pars3", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rule)")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

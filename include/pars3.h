@@ -1,0 +1,143 @@
+/*
+ * pars3.h -- C ABI of libpars3.so, the B200 PARS3 skew-symmetric SpMV path.
+ *
+ * The reference (arxiv/paper_2407_17651, package `skewspmv`) is pure Python
+ * whose "native" layer is a set of numba-jitted kernels called with flat
+ * numpy arrays.  Each entry point below replaces one of those native
+ * kernels (or one numpy preprocessing stage) and is bound from Python with
+ * ctypes by paper_2407_17651_b200/_lib.py; INTEGRATION.md shows the binding
+ * a reference maintainer would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch or CUDA types in signatures;
+ *     `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *   - device arrays: int32 indices, float64 values (n, m < 2^31 at every
+ *     BASELINE configuration); host preprocessing arrays: int64 pointers,
+ *     int32 indices (the reference uses int64 throughout; parity is by value);
+ *   - every function returns PARS3_OK (0) or a negative PARS3_ERR_* code and
+ *     never throws across the ABI; pars3_last_error() gives the message of
+ *     the last failure on the calling thread;
+ *   - sign convention D1 (formats.py:14-18): stored off_diags[k] is the
+ *     LOWER value A[i, col_ind[k]] (col < i); the upper value is its negation.
+ */
+#ifndef PARS3_H
+#define PARS3_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARS3_OK 0
+#define PARS3_ERR_ARG (-1)      /* maps to ValueError */
+#define PARS3_ERR_CUDA (-2)     /* maps to RuntimeError */
+#define PARS3_ERR_STRUCT (-3)   /* maps to StructuralError */
+#define PARS3_ERR_NOMEM (-4)    /* maps to MemoryError */
+
+const char *pars3_last_error(void);
+int pars3_abi_version(void);
+
+/* ------------------------------------------------------------------ SpMV */
+
+/* y = A x over a device SSS matrix with the lock-free atomic scheme:
+ * replaces _spmv_atomic (parallel.py:416-427, wrapper spmv_atomic
+ * parallel.py:430-447).  y is overwritten (zeroed on `stream` first).
+ * Result is reproducible only within rounding, as in the reference. */
+int pars3_sss_spmv_atomic(int32_t n, const int32_t *row_ptr, const int32_t *col_ind,
+                          const double *off_diags, const double *diags, const double *x,
+                          double *y, void *stream);
+
+/* Opaque device plan: the GPU layout derived once from a split (or a full
+ * SSS matrix) and reused by every product. */
+typedef struct pars3_plan pars3_plan;
+
+/* Device view of a BandSplit (split.py:58-113).  All pointers are device
+ * pointers; outer triplets sorted by (row, col) as split_bands leaves them. */
+typedef struct pars3_split_view {
+    int32_t n;
+    int32_t beta;
+    const double *diag;        /* [n]   */
+    const int32_t *mid_ptr;    /* [n+1] */
+    const int32_t *mid_col;    /* [mid_count] */
+    const double *mid_val;     /* [mid_count] */
+    int32_t mid_count;
+    const int32_t *outer_row;  /* [outer_count] */
+    const int32_t *outer_col;
+    const double *outer_val;
+    int32_t outer_count;
+} pars3_split_view;
+
+/* Build the device plan for a split: replaces the layout half of
+ * split_bands + classify_conflicts (split.py:116-141, 303-361) on the GPU.
+ * `p`/`block_start` (host, int64[p+1], from partition_rows split.py:173-188)
+ * fix the row-block ownership used by the multi-GPU path; a single-GPU plan
+ * may pass p = 1.  The split's arrays must outlive the plan. */
+int pars3_plan_create(const pars3_split_view *split, int32_t p, const int64_t *block_start,
+                      pars3_plan **out, void *stream);
+
+/* y = A x through a plan: replaces _pars3 (parallel.py:60-120, wrapper
+ * spmv_pars3 parallel.py:136-183).  y is overwritten. */
+int pars3_plan_spmv(pars3_plan *plan, const double *x, double *y, void *stream);
+
+/* y = A x and *dot = <y, w> in one pass (MRS-style step; no reference
+ * counterpart: the reference stops at the product).  `dot` is
+ * a device pointer to one double; w may equal x. */
+int pars3_plan_spmv_dot(pars3_plan *plan, const double *x, double *y, const double *w,
+                        double *dot, void *stream);
+
+/* Number of libpars3 kernels one pars3_plan_spmv (with_dot = 0) or
+ * pars3_plan_spmv_dot (with_dot = 1) call launches (memsets excluded). */
+int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *count);
+
+/* Device bytes held by the plan (its derived arrays, not the split's). */
+int pars3_plan_bytes(const pars3_plan *plan, int64_t *bytes);
+int pars3_plan_destroy(pars3_plan *plan);
+
+/* --------------------------------------------- host-native preprocessing */
+
+/* Symmetrised off-diagonal adjacency of an SSS pattern: replaces
+ * pattern_from_coo (reorder.py:103-117) for skyline input.  indptr[n+1],
+ * indices[2*nnz]; neighbours ascending. */
+int pars3_pattern_from_lower(int64_t n, const int64_t *row_ptr, const int32_t *col_ind,
+                             int64_t *indptr, int32_t *indices);
+
+/* Reverse Cuthill-McKee labels forward[old] = new: replaces rcm_order
+ * (reorder.py:251-286) bit-exactly, computed level-synchronously with
+ * `nthreads` threads (<= 0: all). */
+int pars3_rcm_order(int64_t n, const int64_t *indptr, const int32_t *indices, int64_t *forward,
+                    int nthreads);
+
+/* Relabel an SSS matrix: replaces coo_to_sss(apply_permutation(coo, perm))
+ * (reorder.py:289-297, formats.py:413-475) without the COO round trip.
+ * Output arrays sized like the input. */
+int pars3_permute_lower(int64_t n, const int64_t *row_ptr, const int32_t *col_ind,
+                        const double *off_diags, const double *diags, const int64_t *forward,
+                        int64_t *out_row_ptr, int32_t *out_col_ind, double *out_off_diags,
+                        double *out_diags, int nthreads);
+
+/* Middle/outer sizes for split_bands (split.py:116-141). */
+int pars3_split_count(int64_t n, const int64_t *row_ptr, const int32_t *col_ind, int64_t beta,
+                      int64_t *mid_count, int64_t *outer_count);
+
+/* split_bands (split.py:116-141): storage order preserved in both bands. */
+int pars3_split_fill(int64_t n, const int64_t *row_ptr, const int32_t *col_ind,
+                     const double *off_diags, int64_t beta, int64_t *mid_ptr, int32_t *mid_col,
+                     double *mid_val, int32_t *outer_row, int32_t *outer_col, double *outer_val);
+
+/* classify_conflicts (split.py:303-361), the PartitionPlan arrays.  Call
+ * with conflict_idx == NULL to get *conflict_count only; then again with
+ * arrays sized [n] (row_owner, safe_start), [k] (conflict_idx,
+ * conflict_target, apply_order), [p+1] (conflict_ptr, apply_ptr), [p]
+ * (halo_lo). */
+int pars3_classify_conflicts(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
+                             int64_t p, const int64_t *block_start, int64_t *conflict_count,
+                             int64_t *row_owner, int64_t *safe_start, int64_t *conflict_idx,
+                             int64_t *conflict_ptr, int64_t *conflict_target,
+                             int64_t *apply_order, int64_t *apply_ptr, int64_t *halo_lo);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARS3_H */

@@ -1,0 +1,116 @@
+"""ctypes binding of libpars3.so (the C ABI declared in include/pars3.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2407_17651_b200/csrc``).  There is no fallback: if it is
+missing, every entry point raises.  Device pointers come from torch CUDA
+tensors (``data_ptr()``), the stream from ``torch.cuda.current_stream()``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_build", "libpars3.so")
+
+PARS3_OK = 0
+PARS3_ERR_ARG = -1
+PARS3_ERR_CUDA = -2
+PARS3_ERR_STRUCT = -3
+PARS3_ERR_NOMEM = -4
+
+_c_i32 = ctypes.c_int32
+_c_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+
+
+class SplitView(ctypes.Structure):
+    """Mirror of ``pars3_split_view`` (include/pars3.h)."""
+
+    _fields_ = [
+        ("n", _c_i32), ("beta", _c_i32), ("diag", _vp), ("mid_ptr", _vp), ("mid_col", _vp),
+        ("mid_val", _vp), ("mid_count", _c_i32), ("outer_row", _vp), ("outer_col", _vp),
+        ("outer_val", _vp), ("outer_count", _c_i32),
+    ]
+
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "pars3_last_error": (ctypes.c_char_p, []),
+    "pars3_abi_version": (ctypes.c_int, []),
+    "pars3_sss_spmv_atomic": (ctypes.c_int, [_c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pars3_plan_create": (ctypes.c_int, [ctypes.POINTER(SplitView), _c_i32, _vp,
+                                         ctypes.POINTER(_vp), _vp]),
+    "pars3_plan_spmv": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "pars3_plan_spmv_dot": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "pars3_plan_bytes": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i64)]),
+    "pars3_plan_kernel_count": (ctypes.c_int, [_vp, _c_i32, ctypes.POINTER(_c_i32)]),
+    "pars3_plan_destroy": (ctypes.c_int, [_vp]),
+    "pars3_pattern_from_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
+    "pars3_rcm_order": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, ctypes.c_int]),
+    "pars3_permute_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                           ctypes.c_int]),
+    "pars3_split_count": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, ctypes.POINTER(_c_i64),
+                                         ctypes.POINTER(_c_i64)]),
+    "pars3_split_fill": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _vp,
+                                        _vp]),
+    "pars3_classify_conflicts": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp,
+                                                ctypes.POINTER(_c_i64), _vp, _vp, _vp, _vp, _vp,
+                                                _vp, _vp, _vp]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load():
+    """Load libpars3.so once; raise if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"libpars3.so not found at {LIB_PATH}: build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map a C return code to the reference's exception types."""
+    if rc == PARS3_OK:
+        return
+    msg = load().pars3_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == PARS3_ERR_ARG:
+        raise ValueError(msg)
+    if rc == PARS3_ERR_STRUCT:
+        from .formats import StructuralError
+        raise StructuralError(msg)
+    if rc == PARS3_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def ptr(a) -> int | None:
+    """Address of a numpy array or torch tensor (None for None/empty)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data if a.size else None
+    return a.data_ptr() if a.numel() else None
+
+
+def stream_ptr(stream=None) -> int | None:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream or None

@@ -1,0 +1,131 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden outputs.
+
+Contract (north star, SPEC.md D14, reference test_acceptance.py:101-130):
+``||y - y_ref||_inf / max(1, ||y_ref||_inf) <= 1e-12`` with ``y_ref`` the
+reference's serial SSS product.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2407_17651_b200 as P
+from conftest import mixed_tol, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2407_17651_b200 import _lib
+    _lib.load()
+
+
+def _sss(g):
+    return P.SssMatrix(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
+
+
+def test_worked_example_exact(golden_corpus):
+    g = golden_corpus["tiny4"]
+    m = _sss(g)
+    s = P.split_bands(m, 2)
+    plan, _ = P.classify_conflicts(s, P.partition_rows(4, 2))
+    y = P.spmv_pars3(s, plan, np.ones(4))
+    assert y.tolist() == [-7.0, -1.0, 2.0, 6.0]
+    assert P.spmv_serial(m, np.ones(4)).tolist() == [-7.0, -1.0, 2.0, 6.0]
+
+
+def test_corpus_all_betas_and_workers(golden_corpus):
+    for name, g in golden_corpus.items():
+        m = _sss(g)
+        for beta in g.betas:
+            s = P.split_bands(m, beta)
+            for p in g.ps():
+                plan, _ = P.classify_conflicts(s, P.partition_rows(m.n, p))
+                y = P.spmv_pars3(s, plan, g.x)
+                assert np.max(np.abs(y - g.y_serial), initial=0.0) <= mixed_tol(g.y_serial, TOL), \
+                    (name, beta, p)
+                # and against the reference's own pars3 output
+                assert rel_err(y, g.y_pars3(beta, p)) <= TOL, (name, beta, p)
+
+
+def test_spmv_serial_and_atomic_corpus(golden_corpus):
+    for name, g in golden_corpus.items():
+        m = _sss(g)
+        assert rel_err(P.spmv_serial(m, g.x), g.y_serial) <= TOL, name
+        assert rel_err(P.spmv_atomic(m, g.x, 4), g.y_serial) <= TOL, name
+        assert rel_err(P.spmv_serial(m, g.x), g.y_dense) <= 1e-13 * 10, name
+
+
+def test_c1_against_golden(golden_c1):
+    z = golden_c1
+    m = P.SssMatrix(int(z["n"]), z["row_ptr"], z["col_ind"], z["off_diags"], z["diags"])
+    for b in (int(z["beta"]), int(z["bandwidth"])):
+        s = P.split_bands(m, b)
+        for p in (1, 2, 4, 8):
+            plan, _ = P.classify_conflicts(s, P.partition_rows(m.n, p))
+            assert rel_err(P.spmv_pars3(s, plan, z["x"]), z["y_serial"]) <= TOL, (b, p)
+
+
+def test_torch_in_torch_out(golden_corpus):
+    import torch
+    g = golden_corpus["gen500"]
+    m = _sss(g)
+    s = P.split_bands(m, 8)
+    plan, _ = P.classify_conflicts(s, P.partition_rows(m.n, 4))
+    xd = torch.from_numpy(g.x).cuda()
+    y = P.spmv_pars3(s, plan, xd)
+    assert isinstance(y, torch.Tensor) and y.is_cuda
+    assert rel_err(y.cpu().numpy(), g.y_serial) <= TOL
+
+
+def test_errors_match_reference(golden_corpus):
+    g = golden_corpus["tiny4"]
+    m = _sss(g)
+    s2, s3 = P.split_bands(m, 2), P.split_bands(m, 3)
+    plan, _ = P.classify_conflicts(s2, P.partition_rows(4, 2))
+    with pytest.raises(ValueError):
+        P.spmv_pars3(s3, plan, np.ones(4))
+    with pytest.raises(ValueError):
+        P.spmv_pars3(s2, plan, np.ones(4), p=3)
+    with pytest.raises(ValueError):
+        P.spmv_pars3(s2, plan, np.ones(5))
+    with pytest.raises(ValueError):
+        P.spmv_atomic(m, np.ones(4), 0)
+
+
+def _pipeline(g, beta=None, p=1):
+    m0 = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
+    m = P.permute_sss(m0, P.rcm_order(P.pattern_from_sss(m0)))
+    if beta is None:
+        beta = P.default_beta(m.n, P.compute_bandwidth(m))
+    s = P.split_bands(m, beta)
+    plan, _ = P.classify_conflicts(s, P.partition_rows(m.n, p))
+    return m, s, plan
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
+def test_baseline_configs_full_size(cfg, oracle):
+    """Every BASELINE configuration at full size against the oracle's serial
+    product (itself pinned to the reference, test_oracle_golden.py)."""
+    from paper_2407_17651_b200 import generators as G
+    g = G.make_config(cfg)
+    m, s, plan = _pipeline(g, p=8)
+    x = G.make_x(m.n, G.CONFIGS[cfg]["seed_x"])
+    y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x)
+    y = P.spmv_pars3(s, plan, x)
+    assert rel_err(y, y_ref) <= TOL, cfg
+
+
+def test_skew_identity_large():
+    """x . (S x) = 0 for strict skew S (reference test_acceptance.py:133-160)."""
+    from paper_2407_17651_b200 import generators as G
+    g = G.stencil27(48, seed_val=3)
+    m, s, plan = _pipeline(g)
+    x = G.make_x(m.n, 4)
+    y = P.spmv_pars3(s, plan, x)
+    assert abs(float(x @ y)) <= 1e-10 * float(x @ x) * float(np.max(np.abs(m.off_diags)))
