@@ -52,29 +52,39 @@ int pars3_sss_spmv_atomic(int32_t n, const int32_t *row_ptr, const int32_t *col_
  * SSS matrix) and reused by every product. */
 typedef struct pars3_plan pars3_plan;
 
-/* Device view of a BandSplit (split.py:58-113).  All pointers are device
- * pointers; outer triplets sorted by (row, col) as split_bands leaves them. */
+/* Host view of a BandSplit (split.py:58-113): the arrays exactly as the
+ * Python BandSplit holds them (int64 pointers, int32 indices, fp64 values);
+ * outer triplets sorted by (row, col) as split_bands leaves them. */
 typedef struct pars3_split_view {
-    int32_t n;
-    int32_t beta;
+    int64_t n;
+    int64_t beta;
     const double *diag;        /* [n]   */
-    const int32_t *mid_ptr;    /* [n+1] */
-    const int32_t *mid_col;    /* [mid_count] */
-    const double *mid_val;     /* [mid_count] */
-    int32_t mid_count;
+    const int64_t *mid_ptr;    /* [n+1] */
+    const int32_t *mid_col;    /* [mid_ptr[n]] */
+    const double *mid_val;
+    int64_t outer_count;
     const int32_t *outer_row;  /* [outer_count] */
     const int32_t *outer_col;
     const double *outer_val;
-    int32_t outer_count;
 } pars3_split_view;
 
-/* Build the device plan for a split: replaces the layout half of
- * split_bands + classify_conflicts (split.py:116-141, 303-361) on the GPU.
- * `p`/`block_start` (host, int64[p+1], from partition_rows split.py:173-188)
- * fix the row-block ownership used by the multi-GPU path; a single-GPU plan
- * may pass p = 1.  The split's arrays must outlive the plan. */
-int pars3_plan_create(const pars3_split_view *split, int32_t p, const int64_t *block_start,
-                      pars3_plan **out, void *stream);
+/* Tiling knobs of the device plan; 0 (or NULL options) = default. */
+typedef struct pars3_plan_options {
+    int32_t tile_rows;    /* rows per tile before splitting (2048) */
+    int32_t local_slots;  /* shared-memory window slots per tile (6144) */
+    int32_t seg_max;      /* max entries per row segment (64) */
+    int32_t gap;          /* merge column runs separated by <= gap slots (8); -1 = default */
+} pars3_plan_options;
+
+/* Build the device plan of a split on the current device: replaces the
+ * per-call setup of _pars3 (parallel.py:136-183).  The split's diagonal,
+ * middle and outer entries are re-tiled into row tiles with shared-memory
+ * column windows and uploaded; the host arrays may be freed
+ * afterwards.  `p`/`block_start` (host int64[p+1], partition_rows
+ * split.py:173-188) record the row-block ownership for the multi-GPU path;
+ * a single-GPU plan passes p = 1. */
+int pars3_plan_create(const pars3_split_view *split, const pars3_plan_options *options,
+                      int32_t p, const int64_t *block_start, pars3_plan **out, void *stream);
 
 /* y = A x through a plan: replaces _pars3 (parallel.py:60-120, wrapper
  * spmv_pars3 parallel.py:136-183).  y is overwritten. */
@@ -90,8 +100,12 @@ int pars3_plan_spmv_dot(pars3_plan *plan, const double *x, double *y, const doub
  * pars3_plan_spmv_dot (with_dot = 1) call launches (memsets excluded). */
 int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *count);
 
-/* Device bytes held by the plan (its derived arrays, not the split's). */
+/* Device bytes held by the plan. */
 int pars3_plan_bytes(const pars3_plan *plan, int64_t *bytes);
+
+/* stats[8] = {tiles, slices, padded slots, stored entries, windows,
+ * max local slots, grid CTAs, device bytes}. */
+int pars3_plan_stats(const pars3_plan *plan, int64_t *stats);
 int pars3_plan_destroy(pars3_plan *plan);
 
 /* --------------------------------------------- host-native preprocessing */

@@ -28,13 +28,20 @@ _vp = ctypes.c_void_p
 
 
 class SplitView(ctypes.Structure):
-    """Mirror of ``pars3_split_view`` (include/pars3.h)."""
+    """Mirror of ``pars3_split_view`` (include/pars3.h): host arrays."""
 
     _fields_ = [
-        ("n", _c_i32), ("beta", _c_i32), ("diag", _vp), ("mid_ptr", _vp), ("mid_col", _vp),
-        ("mid_val", _vp), ("mid_count", _c_i32), ("outer_row", _vp), ("outer_col", _vp),
-        ("outer_val", _vp), ("outer_count", _c_i32),
+        ("n", _c_i64), ("beta", _c_i64), ("diag", _vp), ("mid_ptr", _vp), ("mid_col", _vp),
+        ("mid_val", _vp), ("outer_count", _c_i64), ("outer_row", _vp), ("outer_col", _vp),
+        ("outer_val", _vp),
     ]
+
+
+class PlanOptions(ctypes.Structure):
+    """Mirror of ``pars3_plan_options``."""
+
+    _fields_ = [("tile_rows", _c_i32), ("local_slots", _c_i32), ("seg_max", _c_i32),
+                ("gap", _c_i32)]
 
 
 # name -> (restype, argtypes)
@@ -42,11 +49,12 @@ _SIGS = {
     "pars3_last_error": (ctypes.c_char_p, []),
     "pars3_abi_version": (ctypes.c_int, []),
     "pars3_sss_spmv_atomic": (ctypes.c_int, [_c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "pars3_plan_create": (ctypes.c_int, [ctypes.POINTER(SplitView), _c_i32, _vp,
-                                         ctypes.POINTER(_vp), _vp]),
+    "pars3_plan_create": (ctypes.c_int, [ctypes.POINTER(SplitView), ctypes.POINTER(PlanOptions),
+                                         _c_i32, _vp, ctypes.POINTER(_vp), _vp]),
     "pars3_plan_spmv": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "pars3_plan_spmv_dot": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_plan_bytes": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i64)]),
+    "pars3_plan_stats": (ctypes.c_int, [_vp, _vp]),
     "pars3_plan_kernel_count": (ctypes.c_int, [_vp, _c_i32, ctypes.POINTER(_c_i32)]),
     "pars3_plan_destroy": (ctypes.c_int, [_vp]),
     "pars3_pattern_from_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),

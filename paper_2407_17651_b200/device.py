@@ -1,12 +1,12 @@
-"""Device residency: upload a split once, build the GPU plan once, reuse both.
+"""Device residency: build the GPU plan once per split, reuse it for every product.
 
-``Pars3Operator`` is the object the hot loop holds: device copies of the
-split's arrays (int32 indices, float64 values) plus the opaque native plan
-(libpars3 ``pars3_plan``), with ``matvec`` / ``matvec_dot`` entry points
-over device tensors and no host round trip.  The reference has no such
-object because its arrays already live where its kernels run; here the
-upload is the analogue of the numba first-call cost (bench.py:79-86 keeps
-it out of the clock).
+``Pars3Operator`` is the object the hot loop holds: the opaque native plan
+(libpars3 ``pars3_plan``: the split re-tiled into row tiles with shared-
+memory column windows, uploaded once) with ``matvec`` / ``matvec_dot``
+entry points over device tensors and no host round trip.  The reference
+has no such object because its arrays already live where its kernels run;
+building it is the analogue of the numba first-call cost that
+bench.py:79-86 of the reference keeps out of the clock.
 """
 
 from __future__ import annotations
@@ -17,7 +17,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["require_cuda", "Pars3Operator", "operator_for_split", "operator_for_sss"]
+__all__ = ["require_cuda", "Pars3Operator", "SssDevice", "operator_for_split", "operator_for_sss",
+           "sss_device"]
 
 
 def require_cuda():
@@ -29,44 +30,39 @@ def require_cuda():
     return torch
 
 
-def _dev(a, dtype, torch, device):
-    t = torch.from_numpy(np.ascontiguousarray(a)).to(dtype)
-    return t.to(device, non_blocking=False)
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
 
 
 class Pars3Operator:
     """y = A x on one GPU for a (diag, middle, outer) decomposition of A."""
 
     def __init__(self, n, beta, diag, mid_ptr, mid_col, mid_val, outer_row, outer_col, outer_val,
-                 p=1, block_start=None, device=None):
+                 p=1, block_start=None, device=None, options=None):
         torch = require_cuda()
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.n = int(n)
         self.beta = int(beta)
         self.p = int(p)
-        d = self.device
-        self.diag = _dev(diag, torch.float64, torch, d)
-        self.mid_ptr = _dev(mid_ptr, torch.int32, torch, d)
-        self.mid_col = _dev(mid_col, torch.int32, torch, d)
-        self.mid_val = _dev(mid_val, torch.float64, torch, d)
-        self.outer_row = _dev(outer_row, torch.int32, torch, d)
-        self.outer_col = _dev(outer_col, torch.int32, torch, d)
-        self.outer_val = _dev(outer_val, torch.float64, torch, d)
-        self.mid_count = int(self.mid_col.numel())
-        self.outer_count = int(self.outer_col.numel())
-        self.nnz = self.mid_count + self.outer_count
-        view = _lib.SplitView(
-            self.n, self.beta, _lib.ptr(self.diag), _lib.ptr(self.mid_ptr), _lib.ptr(self.mid_col),
-            _lib.ptr(self.mid_val), self.mid_count, _lib.ptr(self.outer_row),
-            _lib.ptr(self.outer_col), _lib.ptr(self.outer_val), self.outer_count)
-        bs = np.ascontiguousarray(block_start if block_start is not None else [0, self.n],
-                                  dtype=np.int64)
+        host = dict(diag=_c(diag, np.float64), mid_ptr=_c(mid_ptr, np.int64),
+                    mid_col=_c(mid_col, np.int32), mid_val=_c(mid_val, np.float64),
+                    outer_row=_c(outer_row, np.int32), outer_col=_c(outer_col, np.int32),
+                    outer_val=_c(outer_val, np.float64))
+        self.nnz = int(host["mid_col"].size + host["outer_col"].size)
+        view = _lib.SplitView(self.n, self.beta, _lib.ptr(host["diag"]), _lib.ptr(host["mid_ptr"]),
+                              _lib.ptr(host["mid_col"]), _lib.ptr(host["mid_val"]),
+                              int(host["outer_col"].size), _lib.ptr(host["outer_row"]),
+                              _lib.ptr(host["outer_col"]), _lib.ptr(host["outer_val"]))
+        opts = _lib.PlanOptions(*(options or (0, 0, 0, -1)))
+        bs = _c(block_start if block_start is not None else [0, self.n], np.int64)
         handle = ctypes.c_void_p()
         L = _lib.load()
         with torch.cuda.device(self.device):
-            _lib.check(L.pars3_plan_create(ctypes.byref(view), self.p, _lib.ptr(bs),
-                                           ctypes.byref(handle), _lib.stream_ptr()),
+            _lib.check(L.pars3_plan_create(ctypes.byref(view), ctypes.byref(opts), self.p,
+                                           _lib.ptr(bs), ctypes.byref(handle), None),
                        "pars3_plan_create")
         self._handle = handle
         self._L = L
@@ -81,10 +77,12 @@ class Pars3Operator:
         return y
 
     def matvec_dot(self, x, w, y=None, dot=None, stream=None):
-        """y = A x and dot = <y, w> (device scalar tensor) in one pass."""
+        """y = A x and dot = <y, w> (device scalar tensor); ``w`` may be ``y``."""
         t = self.torch
         if y is None:
             y = t.empty(self.n, dtype=t.float64, device=self.device)
+        if w is None:
+            w = y
         if dot is None:
             dot = t.empty(1, dtype=t.float64, device=self.device)
         _lib.check(self._L.pars3_plan_spmv_dot(self._handle, _lib.ptr(x), _lib.ptr(y),
@@ -102,6 +100,13 @@ class Pars3Operator:
         _lib.check(self._L.pars3_plan_bytes(self._handle, ctypes.byref(b)))
         return int(b.value)
 
+    def stats(self) -> dict:
+        a = np.zeros(8, dtype=np.int64)
+        _lib.check(self._L.pars3_plan_stats(self._handle, _lib.ptr(a)))
+        keys = ("tiles", "slices", "padded_slots", "entries", "windows", "max_local", "grid",
+                "device_bytes")
+        return {k: int(v) for k, v in zip(keys, a)}
+
     def close(self):
         if getattr(self, "_handle", None) is not None and self._handle.value:
             self._L.pars3_plan_destroy(self._handle)
@@ -114,32 +119,59 @@ class Pars3Operator:
             pass
 
 
-def operator_for_split(s, p=1, block_start=None, device=None) -> Pars3Operator:
-    """Operator for a BandSplit, cached on the split object per (p, device)."""
-    key = (int(p), str(device))
-    cache = getattr(s, "_device", None)
+class SssDevice:
+    """Device copy of a whole SssMatrix (int32 row_ptr/col_ind) for the
+    atomic comparison kernel."""
+
+    def __init__(self, m, device=None):
+        torch = require_cuda()
+        self.device = torch.device(device if device is not None else "cuda")
+        self.n = m.n
+        self.row_ptr = torch.from_numpy(_c(m.row_ptr, np.int32)).to(self.device)
+        self.col_ind = torch.from_numpy(_c(m.col_ind, np.int32)).to(self.device)
+        self.off_diags = torch.from_numpy(_c(m.off_diags, np.float64)).to(self.device)
+        self.diags = torch.from_numpy(_c(m.diags, np.float64)).to(self.device)
+
+
+def _cache(obj):
+    cache = getattr(obj, "_device", None)
     if cache is None:
         cache = {}
-        object.__setattr__(s, "_device", cache)
+        object.__setattr__(obj, "_device", cache)
+    return cache
+
+
+def operator_for_split(s, p=1, block_start=None, device=None, options=None) -> Pars3Operator:
+    """Operator for a BandSplit, cached on the split object."""
+    key = ("split", int(p), str(device), tuple(options) if options else None)
+    cache = _cache(s)
     op = cache.get(key)
     if op is None:
         op = Pars3Operator(s.n, s.beta, s.diag, s.mid_ptr, s.mid_col, s.mid_val, s.outer_row,
-                           s.outer_col, s.outer_val, p=p, block_start=block_start, device=device)
+                           s.outer_col, s.outer_val, p=p, block_start=block_start, device=device,
+                           options=options)
         cache[key] = op
     return op
 
 
-def operator_for_sss(m, device=None) -> Pars3Operator:
-    """Operator for a whole SssMatrix (everything in the band, beta = n)."""
-    key = ("sss", str(device))
-    cache = getattr(m, "_device", None)
-    if cache is None:
-        cache = {}
-        object.__setattr__(m, "_device", cache)
+def operator_for_sss(m, device=None, options=None) -> Pars3Operator:
+    """Operator for a whole SssMatrix (every entry in the band, beta = n)."""
+    key = ("sss", str(device), tuple(options) if options else None)
+    cache = _cache(m)
     op = cache.get(key)
     if op is None:
         e = np.zeros(0, np.int32)
         op = Pars3Operator(m.n, max(1, m.n), m.diags, m.row_ptr, m.col_ind, m.off_diags, e, e,
-                           np.zeros(0), device=device)
+                           np.zeros(0), device=device, options=options)
         cache[key] = op
     return op
+
+
+def sss_device(m, device=None) -> SssDevice:
+    key = ("sssdev", str(device))
+    cache = _cache(m)
+    d = cache.get(key)
+    if d is None:
+        d = SssDevice(m, device)
+        cache[key] = d
+    return d

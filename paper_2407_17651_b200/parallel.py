@@ -56,9 +56,9 @@ def spmv_atomic(m: SssMatrix, x, t: int = 1, out=None):
     Reproducible within rounding only."""
     if t < 1:
         raise ValueError(f"worker count must be at least 1, got {t}")
-    from .device import operator_for_sss, require_cuda
+    from .device import require_cuda, sss_device
     torch = require_cuda()
-    op = operator_for_sss(m)
+    op = sss_device(m)
     numpy_in = not isinstance(x, torch.Tensor)
     if numpy_in:
         xv = as_vector(x, m.n)
@@ -71,6 +71,6 @@ def spmv_atomic(m: SssMatrix, x, t: int = 1, out=None):
         xd = x.to(device=op.device, dtype=torch.float64).contiguous()
     y = out if out is not None else torch.empty(m.n, dtype=torch.float64, device=op.device)
     _lib.check(_lib.load().pars3_sss_spmv_atomic(
-        m.n, _lib.ptr(op.mid_ptr), _lib.ptr(op.mid_col), _lib.ptr(op.mid_val),
-        _lib.ptr(op.diag), _lib.ptr(xd), _lib.ptr(y), _lib.stream_ptr()), "spmv_atomic")
+        m.n, _lib.ptr(op.row_ptr), _lib.ptr(op.col_ind), _lib.ptr(op.off_diags),
+        _lib.ptr(op.diags), _lib.ptr(xd), _lib.ptr(y), _lib.stream_ptr()), "spmv_atomic")
     return y.cpu().numpy() if numpy_in else y

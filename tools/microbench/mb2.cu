@@ -15,7 +15,7 @@ __global__ void k(double* out, int iters, int span){
   #pragma unroll 4
   for(int it=0;it<iters;it++){
     uint32_t a;
-    if(OP==0||OP==2||OP==4) a = ((w*37+it)*32 + lane) & (span-1);           // sequential within warp
+    if(OP==0||OP==2||OP==4||OP==10||OP==11) a = ((w*37+it)*32 + lane) & (span-1);           // sequential within warp
     else { seed = seed*1664525u + 1013904223u; a = (seed>>7) & (span-1); }                                            // random
     if(OP==0||OP==1) acc += s[a];                                            // LDS.64
     else if(OP==2||OP==3) s[a] = acc + it;                                   // STS.64
@@ -23,18 +23,20 @@ __global__ void k(double* out, int iters, int span){
     else if(OP==6) atomicAdd(s+a, 1.0);                                      // CAS f64
     else if(OP==7) acc += __shfl_xor_sync(0xffffffff, acc+it, 1);            // SHFL double
     else if(OP==8) { s[a] += 1.0; }
-    else if(OP==9) { acc += (double)(a&7); }                                          // LDS+STS RMW random
+    else if(OP==9) { acc += (double)(a&7); }
+    else if(OP==10) atomicAdd(s+a, 1.0);
+    else if(OP==11) { s[a] += 1.0; }                                          // LDS+STS RMW random
   }
   if(acc==1.2345) out[blockIdx.x]=acc;
 }
 int main(){
   cudaEvent_t e0,e1; cudaEventCreate(&e0); cudaEventCreate(&e1); float ms;
   double* out; cudaMalloc(&out, 1<<20);
-  const char* names[]={"LDS.64 seq","LDS.64 rand","STS.64 seq","STS.64 rand","ATOMS.ADD.32 seq","ATOMS.ADD.32 rand","CAS-f64 rand","SHFL f64","RMW f64 rand","ALU only"};
+  const char* names[]={"LDS.64 seq","LDS.64 rand","STS.64 seq","STS.64 rand","ATOMS.ADD.32 seq","ATOMS.ADD.32 rand","CAS-f64 rand","SHFL f64","RMW f64 rand","ALU only","CAS-f64 seq","RMW f64 seq"};
   int sms=148, iters=4096, span=4096;
   for(int bs: {256, 1024}){
     int grid=sms*(2048/bs);
-    for(int op=0;op<10;op++){
+    for(int op=0;op<12;op++){
       auto launch=[&](){
         switch(op){
           case 0: k<0><<<grid,bs,span*8>>>(out,iters,span); break;
@@ -47,6 +49,8 @@ int main(){
           case 7: k<7><<<grid,bs,span*8>>>(out,iters,span); break;
           case 8: k<8><<<grid,bs,span*8>>>(out,iters,span); break;
           case 9: k<9><<<grid,bs,span*8>>>(out,iters,span); break;
+          case 10: k<10><<<grid,bs,span*8>>>(out,iters,span); break;
+          case 11: k<11><<<grid,bs,span*8>>>(out,iters,span); break;
         }};
       launch(); cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
       cudaEventElapsedTime(&ms,e0,e1);
