@@ -74,6 +74,8 @@ typedef struct pars3_plan_options {
     int32_t local_slots;  /* shared-memory window slots per tile (6144) */
     int32_t seg_max;      /* max entries per row segment (64) */
     int32_t gap;          /* merge column runs separated by <= gap slots (8); -1 = default */
+    int32_t mode;         /* 0 auto, 1 ordered (owners store, later tiles reduce after the
+                             owner's flag), 2 accumulate (y zeroed, all contributions reduce) */
 } pars3_plan_options;
 
 /* Build the device plan of a split on the current device: replaces the
@@ -103,10 +105,18 @@ int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *c
 /* Device bytes held by the plan. */
 int pars3_plan_bytes(const pars3_plan *plan, int64_t *bytes);
 
-/* stats[8] = {tiles, slices, padded slots, stored entries, windows,
- * max local slots, grid CTAs, device bytes}. */
+/* stats[10] = {tiles, slices, padded slots, stored entries, windows,
+ * max local slots, grid CTAs, device bytes, list-mode tiles, accumulate}. */
 int pars3_plan_stats(const pars3_plan *plan, int64_t *stats);
 int pars3_plan_destroy(pars3_plan *plan);
+
+/* Debug: host address of the plan's progress-trace buffer (mapped host
+ * memory, 32 int32 per CTA) when created with PARS3_TRACE=1, else NULL. */
+int pars3_plan_trace(const pars3_plan *plan, int32_t **host);
+
+/* Debug: per-phase SM-cycle totals of the tile kernel (created with
+ * PARS3_PHASES=1; claim, windows, stream, store, wait, flush). */
+int pars3_plan_phases(const pars3_plan *plan, int64_t *out6);
 
 /* --------------------------------------------- host-native preprocessing */
 

@@ -41,7 +41,7 @@ class PlanOptions(ctypes.Structure):
     """Mirror of ``pars3_plan_options``."""
 
     _fields_ = [("tile_rows", _c_i32), ("local_slots", _c_i32), ("seg_max", _c_i32),
-                ("gap", _c_i32)]
+                ("gap", _c_i32), ("mode", _c_i32)]
 
 
 # name -> (restype, argtypes)
@@ -57,6 +57,8 @@ _SIGS = {
     "pars3_plan_stats": (ctypes.c_int, [_vp, _vp]),
     "pars3_plan_kernel_count": (ctypes.c_int, [_vp, _c_i32, ctypes.POINTER(_c_i32)]),
     "pars3_plan_destroy": (ctypes.c_int, [_vp]),
+    "pars3_plan_trace": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
+    "pars3_plan_phases": (ctypes.c_int, [_vp, _vp]),
     "pars3_pattern_from_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
     "pars3_rcm_order": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, ctypes.c_int]),
     "pars3_permute_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -14,6 +14,7 @@ namespace pars3 {
 namespace {
 
 struct Rows {
+    int64_t n;
     const int64_t *optr;  // outer row pointer (built here)
     const int32_t *ocol;
     const double *oval;
@@ -43,15 +44,18 @@ struct Draft {
 
 struct Built {               // one draft materialised
     std::vector<int32_t> wlo, wlen, wloff;
-    std::vector<int32_t> slice_base, slice_nslots;
-    std::vector<uint16_t> slice_rowl;
-    std::vector<double> val;
-    std::vector<uint16_t> lidx;
-    int32_t r0, r1, local, own_loff;
-    int64_t nnz;
+    bool list = false;           // explicit column list instead of windows
+    std::vector<int32_t> ucol;
+    std::vector<int64_t> slice_off;  // relative, bytes
+    std::vector<uint8_t> rec;
+    int32_t r0, r1, local, own_loff, max_nslots = 0;
+    int64_t nnz, slots;
 };
 
-void make_windows(std::vector<int32_t> &cols, int32_t gap, Draft &d) {
+// Merge sorted unique columns into dense windows (runs separated by <= gap
+// unused slots).  With `align` the windows are widened to even bounds (the
+// kernel moves them with 16-byte TMA bulk copies), never past column n.
+void make_windows(std::vector<int32_t> &cols, int32_t gap, bool align, int64_t n, Draft &d) {
     std::sort(cols.begin(), cols.end());
     cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
     d.wlo.clear();
@@ -62,6 +66,18 @@ void make_windows(std::vector<int32_t> &cols, int32_t gap, Draft &d) {
         int32_t lo = cols[i], hi = cols[i] + 1;
         size_t j = i + 1;
         while (j < cols.size() && cols[j] - hi <= gap) hi = cols[j++] + 1;
+        if (align) {
+            lo &= ~1;
+            if ((hi & 1) && hi < n) hi++;
+            if (!d.wlo.empty() && lo <= d.wlo.back() + d.wlen.back()) {  // touches the previous
+                const int32_t plo = d.wlo.back();
+                d.local -= d.wlen.back();
+                d.wlen.back() = hi - plo;
+                d.local += hi - plo;
+                i = j;
+                continue;
+            }
+        }
         d.wlo.push_back(lo);
         d.wlen.push_back(hi - lo);
         d.local += hi - lo;
@@ -72,15 +88,26 @@ void make_windows(std::vector<int32_t> &cols, int32_t gap, Draft &d) {
 void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
                  std::vector<Draft> &out, std::vector<int32_t> &scratch) {
     scratch.clear();
+    int64_t segments = 0;
     for (int32_t r = a; r < b; r++) {
         scratch.push_back(r);
         int64_t c = R.count(r);
+        segments += (c + o.seg_max - 1) / o.seg_max;
         for (int64_t k = 0; k < c; k++) scratch.push_back(R.col(r, k));
+    }
+    if (segments > o.max_segments && b - a > 1) {
+        int32_t mid = a + (b - a) / 2;
+        draft_range(R, a, mid, o, out, scratch);
+        draft_range(R, mid, b, o, out, scratch);
+        return;
     }
     Draft d;
     d.r0 = a;
     d.r1 = b;
-    make_windows(scratch, o.gap, d);
+    make_windows(scratch, o.gap, true, R.n, d);
+    // too fragmented for windows: the tile will carry an explicit column
+    // list, so do not pay for gap or alignment slots
+    if ((int)d.wlo.size() > kMaxWindows) make_windows(scratch, 0, false, R.n, d);
     if (d.local <= o.local_slots) {
         out.push_back(std::move(d));
         return;
@@ -106,7 +133,7 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
         scratch.clear();
         scratch.push_back(a);
         for (int64_t k = h.k0; k < h.k1; k++) scratch.push_back(R.col(a, k));
-        make_windows(scratch, 0, h);
+        make_windows(scratch, 0, false, R.n, h);
         out.push_back(std::move(h));
     }
 }
@@ -131,6 +158,12 @@ void materialise(const Rows &R, const Draft &d, const PlanOptions &o, Built &b) 
     b.r1 = d.r1;
     b.local = d.local;
     b.own_loff = local_of(d, b.wloff, d.r0);
+    b.list = (int)d.wlo.size() > kMaxWindows || d.hub >= 0;
+    if (b.list) {
+        b.ucol.reserve(d.local);
+        for (size_t w = 0; w < d.wlo.size(); w++)
+            for (int32_t i = 0; i < d.wlen[w]; i++) b.ucol.push_back(d.wlo[w] + i);
+    }
     // row segments (row, k begin, k end)
     struct Seg {
         int32_t row;
@@ -148,28 +181,33 @@ void materialise(const Rows &R, const Draft &d, const PlanOptions &o, Built &b) 
     std::stable_sort(segs.begin(), segs.end(),
                      [](const Seg &x, const Seg &y) { return (x.ke - x.kb) > (y.ke - y.kb); });
     b.nnz = 0;
-    int64_t base = 0;
+    b.slots = 0;
     for (size_t s0 = 0; s0 < segs.size(); s0 += 32) {
         size_t s1 = std::min(segs.size(), s0 + 32);
-        int32_t nslots = (int32_t)(segs[s0].ke - segs[s0].kb);
-        b.slice_base.push_back((int32_t)base);
-        b.slice_nslots.push_back(nslots);
+        const int32_t nslots = (int32_t)(segs[s0].ke - segs[s0].kb);
+        b.max_nslots = std::max(b.max_nslots, nslots);
+        const size_t off = b.rec.size();
+        b.slice_off.push_back((int64_t)off);
+        b.rec.resize(off + 64 + (size_t)nslots * 320, 0);
+        uint16_t *rowl = reinterpret_cast<uint16_t *>(&b.rec[off]);
+        double *val = reinterpret_cast<double *>(&b.rec[off + 64]);
+        uint16_t *lidx = reinterpret_cast<uint16_t *>(&b.rec[off + 64 + (size_t)nslots * 256]);
         for (size_t l = 0; l < 32; l++)
-            b.slice_rowl.push_back(s0 + l < s1 ? (uint16_t)local_of(d, b.wloff, segs[s0 + l].row)
-                                               : kNoSlot);
-        size_t off = b.val.size();
-        b.val.resize(off + (size_t)nslots * 32, 0.0);
-        b.lidx.resize(off + (size_t)nslots * 32, kNoSlot);
+            rowl[l] = s0 + l < s1 ? (uint16_t)local_of(d, b.wloff, segs[s0 + l].row) : kNoSlot;
+        for (int64_t q = 0; q < (int64_t)nslots * 32; q++) {
+            val[q] = 0.0;
+            lidx[q] = kNoSlot;
+        }
         for (size_t l = 0; l < s1 - s0; l++) {
             const Seg &sg = segs[s0 + l];
             for (int64_t k = sg.kb; k < sg.ke; k++) {
-                size_t pos = off + (size_t)(k - sg.kb) * 32 + l;
-                b.val[pos] = R.val(sg.row, k);
-                b.lidx[pos] = (uint16_t)local_of(d, b.wloff, R.col(sg.row, k));
+                const size_t pos = (size_t)(k - sg.kb) * 32 + l;
+                val[pos] = R.val(sg.row, k);
+                lidx[pos] = (uint16_t)local_of(d, b.wloff, R.col(sg.row, k));
                 b.nnz++;
             }
         }
-        base += (int64_t)nslots * 32;
+        b.slots += (int64_t)nslots * 32;
     }
 }
 
@@ -189,7 +227,7 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
             optr[r + 1]++;
         }
         for (int64_t r = 0; r < n; r++) optr[r + 1] += optr[r];
-        Rows R{optr.data(), outer_col, outer_val, mid_ptr, mid_col, mid_val};
+        Rows R{n, optr.data(), outer_col, outer_val, mid_ptr, mid_col, mid_val};
 
         const int64_t nranges = (n + o.tile_rows - 1) / o.tile_rows;
         std::vector<std::vector<Draft>> drafts(nranges);
@@ -226,27 +264,27 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
         P = HostPlan();
         P.n = n;
         P.tiles.resize(nt);
-        int64_t nw = 0, ns = 0, nv = 0;
+        int64_t nw = 0, ns = 0, nv = 0, nu = 0;
         for (auto &b : built) {
-            nw += (int64_t)b.wlo.size();
-            ns += (int64_t)b.slice_base.size();
-            nv += (int64_t)b.val.size();
+            nu += (int64_t)b.ucol.size();
+            if (!b.list) nw += (int64_t)b.wlo.size();
+            ns += (int64_t)b.slice_off.size();
+            nv += (int64_t)b.rec.size();
         }
-        if (nv >= INT32_MAX) PARS3_FAIL(PARS3_ERR_ARG, "plan too large for int32 slot offsets");
         P.wins.resize(nw);
-        P.slice_base.resize(ns);
-        P.slice_nslots.resize(ns);
-        P.slice_rowl.resize(ns * 32);
-        P.val.resize(nv);
-        P.lidx.resize(nv);
-        std::vector<int64_t> w_off(nt + 1, 0), s_off(nt + 1, 0), v_off(nt + 1, 0);
+        P.ucol.resize(nu);
+        P.slice_off.resize(ns + 1);
+        P.rec.resize(nv);
+        std::vector<int64_t> w_off(nt + 1, 0), s_off(nt + 1, 0), v_off(nt + 1, 0), u_off(nt + 1, 0);
         for (int64_t t = 0; t < nt; t++) {
-            w_off[t + 1] = w_off[t] + (int64_t)built[t].wlo.size();
-            s_off[t + 1] = s_off[t] + (int64_t)built[t].slice_base.size();
-            v_off[t + 1] = v_off[t] + (int64_t)built[t].val.size();
+            w_off[t + 1] = w_off[t] + (built[t].list ? 0 : (int64_t)built[t].wlo.size());
+            u_off[t + 1] = u_off[t] + (int64_t)built[t].ucol.size();
+            P.list_tiles += built[t].list ? 1 : 0;
+            s_off[t + 1] = s_off[t] + (int64_t)built[t].slice_off.size();
+            v_off[t + 1] = v_off[t] + (int64_t)built[t].rec.size();
         }
-        int64_t nnz_total = 0;
-#pragma omp parallel for schedule(dynamic, 16) reduction(+ : nnz_total)
+        int64_t nnz_total = 0, slots_total = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : nnz_total, slots_total)
         for (int64_t t = 0; t < nt; t++) {
             Built &b = built[t];
             TileMeta &m = P.tiles[t];
@@ -258,7 +296,22 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
             m.s1 = (int32_t)s_off[t + 1];
             m.local = b.local;
             m.own_loff = b.own_loff;
-            for (size_t w = 0; w < b.wlo.size(); w++) {
+            m.u0 = b.list ? (int32_t)u_off[t] : -1;
+            m.wt_lo = INT32_MAX;
+            m.wt_hi = -1;
+            m.pad = 0;
+            if (b.list) {
+                std::memcpy(&P.ucol[u_off[t]], b.ucol.data(), b.ucol.size() * sizeof(int32_t));
+                for (size_t w = 0; w < b.wlo.size(); w++) {
+                    int32_t lo = b.wlo[w], hi = b.wlo[w] + b.wlen[w] - 1;
+                    // own rows are the tail of the slot list; exclude them
+                    if (b.r1 > b.r0) hi = std::min(hi, b.r0 - 1);
+                    if (hi < lo) continue;
+                    m.wt_lo = std::min(m.wt_lo, owner_of(lo));
+                    m.wt_hi = std::max(m.wt_hi, owner_of(hi));
+                }
+            }
+            for (size_t w = 0; !b.list && w < b.wlo.size(); w++) {
                 Window &W = P.wins[w_off[t] + w];
                 W.lo = b.wlo[w];
                 W.len = b.wlen[w];
@@ -267,21 +320,19 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
                 W.t_hi = owner_of(b.wlo[w] + b.wlen[w] - 1);
                 W.pad0 = W.pad1 = W.pad2 = 0;
             }
-            for (size_t s = 0; s < b.slice_base.size(); s++) {
-                P.slice_base[s_off[t] + s] = (int32_t)(v_off[t] + b.slice_base[s]);
-                P.slice_nslots[s_off[t] + s] = b.slice_nslots[s];
-            }
-            std::memcpy(&P.slice_rowl[s_off[t] * 32], b.slice_rowl.data(),
-                        b.slice_rowl.size() * sizeof(uint16_t));
-            std::memcpy(&P.val[v_off[t]], b.val.data(), b.val.size() * sizeof(double));
-            std::memcpy(&P.lidx[v_off[t]], b.lidx.data(), b.lidx.size() * sizeof(uint16_t));
+            for (size_t s = 0; s < b.slice_off.size(); s++)
+                P.slice_off[s_off[t] + s] = (v_off[t] + b.slice_off[s]) / 16;
+            std::memcpy(&P.rec[v_off[t]], b.rec.data(), b.rec.size());
             nnz_total += b.nnz;
+            slots_total += b.slots;
             std::vector<int32_t>().swap(b.wlo);
-            std::vector<double>().swap(b.val);
-            std::vector<uint16_t>().swap(b.lidx);
+            std::vector<uint8_t>().swap(b.rec);
         }
         P.nnz = nnz_total;
+        P.slots = slots_total;
+        P.slice_off[ns] = nv / 16;
         for (auto &m : P.tiles) P.max_local = std::max(P.max_local, m.local);
+        for (auto &b : built) P.max_nslots = std::max(P.max_nslots, b.max_nslots);
     } catch (const std::bad_alloc &) {
         PARS3_FAIL(PARS3_ERR_NOMEM, "tile plan: out of host memory");
     }

@@ -8,6 +8,10 @@
 // and the accumulator for y[c] in shared memory.  Entries are stored in
 // SELL-32 slices (32 row segments x nslots, slot-major) as fp64 value +
 // uint16 local column index; padding lanes carry the 0xFFFF sentinel.
+// Each slice is one contiguous RECORD, the unit the kernel's TMA producer
+// streams into shared memory with one bulk copy:
+//     [rowl: 32 x u16][val: nslots x 32 x f64][lidx: nslots x 32 x u16]
+// (64 + 320 * nslots bytes, 16-byte aligned).
 #pragma once
 #include <cstdint>
 #include <vector>
@@ -19,16 +23,23 @@ constexpr uint16_t kNoSlot = 0xFFFF;
 struct PlanOptions {
     int32_t tile_rows = 2048;   // rows per tile before splitting
     int32_t local_slots = 6144; // shared-memory window slots per tile (x + acc = 16 B each)
-    int32_t seg_max = 64;       // max entries per row segment (longer rows are split)
+    int32_t seg_max = 8;        // max entries per row segment (longer rows are split)
     int32_t gap = 8;            // merge column runs separated by <= gap unused slots
+    int32_t max_segments = 16384;  // row segments per tile (the kernel's slice table bound / 32)
+    int32_t mode = 0;           // 0 auto, 1 ordered (owner stores + flags), 2 accumulate (y zeroed, all reductions)
 };
 
-struct TileMeta {     // 8 x int32
-    int32_t r0, r1;   // owned rows
-    int32_t w0, w1;   // window range
-    int32_t s0, s1;   // slice range
-    int32_t local;    // local index space size
-    int32_t own_loff; // local index of row r0 (valid when r1 > r0)
+constexpr int kMaxWindows = 8;  // more windows than this -> explicit column list
+
+struct TileMeta {      // 12 x int32
+    int32_t r0, r1;    // owned rows
+    int32_t w0, w1;    // window range (window mode)
+    int32_t u0;        // offset of the explicit column list (list mode), else -1
+    int32_t s0, s1;    // slice range
+    int32_t local;     // local index space size
+    int32_t own_loff;  // local index of row r0 (valid when r1 > r0)
+    int32_t wt_lo, wt_hi;  // list mode: hull of owner tiles of non-own slots (wt_lo > wt_hi: none)
+    int32_t pad;
 };
 
 struct Window {       // 8 x int32
@@ -41,12 +52,13 @@ struct HostPlan {
     int64_t n = 0;
     std::vector<TileMeta> tiles;
     std::vector<Window> wins;
-    std::vector<int32_t> slice_base;    // first entry (multiple of 32) of each slice
-    std::vector<int32_t> slice_nslots;
-    std::vector<uint16_t> slice_rowl;   // 32 per slice: local index of each lane's row
-    std::vector<double> val;            // slot-major, 32 lanes per slot
-    std::vector<uint16_t> lidx;
+    std::vector<int64_t> slice_off;     // record start of each slice, in 16-byte units (+ end)
+    std::vector<uint8_t> rec;           // slice records (see above)
+    std::vector<int32_t> ucol;          // list-mode tiles: global column of each local slot
     int64_t nnz = 0;                    // stored entries (without padding)
+    int64_t slots = 0;                  // stored slots (with padding)
+    int32_t max_nslots = 0;
+    int32_t list_tiles = 0;
     int32_t max_local = 0;
 };
 

@@ -1,10 +1,11 @@
 // Windowed tile kernel: the single-GPU PARS3 product.
 //
-// One persistent CTA loop; tiles are claimed in ascending order from an
+// One persistent CTA per SM; tiles are claimed in ascending order from an
 // atomic counter.  Per tile:
 //   1. the tile's column windows of x are copied into shared memory (xs) and
 //      the matching accumulators (acc) zeroed;
-//   2. each warp streams SELL-32 slices (fp64 value + uint16 local column):
+//   2. each warp streams its SELL-32 slice records (fp64 value + uint16 local
+//      column) through a private TMA ring (cp.async.bulk + mbarrier):
 //      lane l owns one row segment, keeps its row sum in a register
 //      (+a_ic * x_c, serial.py:56-57) and adds the mirror -a_ic * x_i into
 //      acc[c] (serial.py:58-59) -- both in shared memory, no global atomics;
@@ -20,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -34,24 +37,94 @@ using pars3::Window;
 namespace {
 
 constexpr uint16_t kNo = pars3::kNoSlot;
+// 2 CTAs per SM x 16 warps: the slice loop streams whole records into
+// registers (tools/microbench/mb3.cu: this inner loop alone runs at ~6.7 TB/s
+// on c5-shaped data), and the second CTA overlaps each CTA's per-tile
+// window/flush phases.
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
+constexpr int kMaxTileSlices = 1024;  // per-tile slice offset table in shared memory
+constexpr int kMaxSlots = 8;          // slots per slice (plan seg_max)
 
 struct DevPlan {
     const TileMeta *tiles;
     const Window *wins;
-    const int32_t *sbase;
-    const int32_t *sns;
-    const uint16_t *srowl;
-    const double *val;
-    const uint16_t *lidx;
+    const int64_t *slice_off;  // 16-byte units
+    const uint8_t *rec;
+    const int32_t *ucol;
     const double *diag;
     int32_t *flags;
     int32_t *counter;
     int32_t ntiles;
     int32_t lmax;
+    int32_t stage_bytes;
+    int32_t accumulate;
+    int32_t watchdog;
+    int32_t diag_const;  // 1: every diagonal value equals diag_alpha (strict / shifted skew)
+    double diag_alpha;
+    volatile int32_t *trace;  // mapped host memory, 32 ints per CTA (debug), or null
+    unsigned long long *phase_clk;  // PARS3_PHASES=1: per-phase SM cycles (thread 0 of each CTA)
 };
 
+// debug trace (PARS3_TRACE=1): progress markers readable by the host while the
+// kernel runs; slot 0-3 producer, 4-7 consumer leader, 8+ consumer warps
+#define TRACE(P, slot, v)                                                  \
+    do {                                                                   \
+        if ((P).trace) (P).trace[blockIdx.x * 32 + (slot)] = (int32_t)(v); \
+    } while (0)
+
+__device__ __forceinline__ uint32_t saddr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(saddr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// wait for the phase of `bar` with the given parity; `what`/`tag` feed the
+// debug watchdog (PARS3_WATCHDOG=1)
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, int watchdog = 0,
+                                          int what = 0, int tag = 0) {
+    if (!watchdog) {
+        while (!mbar_try(bar, parity)) {
+        }
+        return;
+    }
+    for (long long it = 0; !mbar_try(bar, parity); it++) {
+        if (it == (1ll << 26)) {
+            if ((threadIdx.x & 31) == 0)
+                printf("pars3 watchdog: block %d warp %d stuck on mbarrier kind %d tag %d parity %u\n",
+                       blockIdx.x, threadIdx.x >> 5, what, tag, parity);
+            return;
+        }
+    }
+}
+// one TMA bulk copy global -> shared, completion counted on `bar`
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes,
+                                          uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            saddr(dst)),
+        "l"(src), "r"(bytes), "r"(saddr(bar))
+        : "memory");
+}
 __device__ __forceinline__ int32_t ld_acquire(const int32_t *p) {
     int32_t v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -62,14 +135,23 @@ __device__ __forceinline__ void st_release(int32_t *p, int32_t v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// local slot -> window (binary search over the tile's window loff)
-__device__ __forceinline__ int find_window(const Window *wins, int w0, int w1, int i) {
-    int lo = w0, hi = w1 - 1;
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (__ldg(&wins[mid].loff) <= i) lo = mid; else hi = mid - 1;
+// Spin until tile u's flag shows this launch's epoch.  With `watchdog` set
+// (PARS3_WATCHDOG=1) a wait that exceeds ~2^26 polls reports and gives up
+// instead of hanging the device (debug aid; results are then invalid).
+__device__ __forceinline__ void wait_flag(const int32_t *flags, int u, int32_t epoch, int t,
+                                          int watchdog) {
+    if (!watchdog) {
+        while (ld_acquire(flags + u) != epoch) {
+        }
+        return;
     }
-    return lo;
+    for (long long it = 0; ld_acquire(flags + u) != epoch; it++) {
+        if (it == (1ll << 26)) {
+            printf("pars3 watchdog: tile %d waits on tile %d (flag %d, epoch %d)\n", t, u,
+                   ld_acquire(flags + u), epoch);
+            return;
+        }
+    }
 }
 
 __device__ __forceinline__ void entry(double v, uint16_t li, double xr, const double *xs,
@@ -80,108 +162,205 @@ __device__ __forceinline__ void entry(double v, uint16_t li, double xr, const do
     }
 }
 
+__device__ __forceinline__ bool tma_window(int lo, int len) { return ((lo | len) & 1) == 0; }
+
+__device__ __forceinline__ void bulk_reduce_add(double *g, const double *s, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(g),
+                 "r"(saddr(s)), "r"(bytes)
+                 : "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 2)
 k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t epoch) {
-    extern __shared__ double sm[];
-    double *xs = sm;
-    double *acc = sm + P.lmax;
+    extern __shared__ __align__(128) uint8_t dyn[];
+    double *xs = reinterpret_cast<double *>(dyn);
+    double *acc = xs + P.lmax;
+    __shared__ int64_t s_off[kMaxTileSlices + 1];
     __shared__ int32_t s_tile;
+    __shared__ __align__(8) uint64_t xbar;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < P.lmax; i += kThreads) acc[i] = 0.0;
+    if (tid == 0) {
+        mbar_init(&xbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // PARS3_PHASES=1: thread 0 accumulates SM cycles per phase (claim,
+    // windows, stream, finish+store, wait, flush)
+    long long clk[6] = {0, 0, 0, 0, 0, 0};
+    long long tprev = clock64();
+#define PHASE(k)                                  \
+    do {                                          \
+        if (P.phase_clk && tid == 0) {            \
+            const long long now = clock64();      \
+            clk[k] += now - tprev;                \
+            tprev = now;                          \
+        }                                         \
+    } while (0)
 
+    __syncthreads();
+    uint32_t xphase = 0;  // completed phases of xbar (window-mode tiles only)
     for (;;) {
         if (tid == 0) s_tile = atomicAdd(P.counter, 1);
         __syncthreads();
+        PHASE(0);
         const int32_t t = s_tile;
         if (t >= P.ntiles) break;
         const TileMeta m = P.tiles[t];
-        const int nw = m.w1 - m.w0;
+        const int nown = m.r1 - m.r0;
+        const int nsl = m.s1 - m.s0;
 
-        // 1. x windows -> shared memory, accumulators cleared
-        if (nw <= 8) {
+        // 1. slice offsets; x over the tile's local slots -> shared memory:
+        //    windows by TMA bulk copies (one round trip for the whole tile),
+        //    odd-aligned windows and list-mode slots by the threads
+        if (m.u0 < 0 && tid == 0) {
+            uint32_t bytes = 0;
+            for (int w = m.w0; w < m.w1; w++) {
+                const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len);
+                if (tma_window(lo, len)) bytes += (uint32_t)len * 8;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_tx(&xbar, bytes);
             for (int w = m.w0; w < m.w1; w++) {
                 const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
                           off = __ldg(&P.wins[w].loff);
-                for (int i = tid; i < len; i += kThreads) {
-                    xs[off + i] = __ldg(x + lo + i);
-                    acc[off + i] = 0.0;
-                }
-            }
-        } else {
-            for (int i = tid; i < m.local; i += kThreads) {
-                const int w = find_window(P.wins, m.w0, m.w1, i);
-                xs[i] = __ldg(x + __ldg(&P.wins[w].lo) + (i - __ldg(&P.wins[w].loff)));
-                acc[i] = 0.0;
+                if (tma_window(lo, len)) bulk_load(xs + off, x + lo, (uint32_t)len * 8, &xbar);
             }
         }
+        for (int i = tid; i <= nsl; i += kThreads) s_off[i] = __ldg(P.slice_off + m.s0 + i);
+        if (m.u0 >= 0) {
+            const int32_t *uc = P.ucol + m.u0;
+            for (int i = tid; i < m.local; i += kThreads) xs[i] = __ldg(x + __ldg(uc + i));
+        } else {
+            for (int w = m.w0; w < m.w1; w++) {
+                const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
+                          off = __ldg(&P.wins[w].loff);
+                if (!tma_window(lo, len))
+                    for (int i = tid; i < len; i += kThreads) xs[off + i] = __ldg(x + lo + i);
+            }
+            mbar_wait(&xbar, (uint32_t)(xphase & 1), P.watchdog, 5, t);
+            xphase++;
+        }
         __syncthreads();
+        PHASE(1);
 
-        // 2. SELL-32 slices: row sums in registers, mirrors into acc
-        for (int s = m.s0 + warp; s < m.s1; s += kWarps) {
-            const int base = __ldg(P.sbase + s), ns = __ldg(P.sns + s);
-            const uint16_t rl = __ldg(P.srowl + s * 32 + lane);
-            const double xr = rl != kNo ? xs[rl] : 0.0;
-            double racc = 0.0;
-            const double *vp = P.val + base + lane;
-            const uint16_t *ip = P.lidx + base + lane;
-            int j = 0;
-            for (; j + 4 <= ns; j += 4, vp += 128, ip += 128) {
-                double v[4];
-                uint16_t li[4];
+        // 2. records: each lane owns one row segment of a slice; row sums in
+        //    registers, mirrors into acc (shared-memory fp64 atomics)
+        for (int i = warp; i < nsl; i += kWarps) {
+            const uint8_t *rp = P.rec + s_off[i] * 16;
+            const int ns = (int)(((s_off[i + 1] - s_off[i]) * 16 - 64) / 320);
+            const uint16_t rl = __ldcs(reinterpret_cast<const uint16_t *>(rp) + lane);
+            const double *vp = reinterpret_cast<const double *>(rp + 64) + lane;
+            const uint16_t *ip = reinterpret_cast<const uint16_t *>(rp + 64 + ns * 256) + lane;
+            double v[kMaxSlots];
+            uint16_t li[kMaxSlots];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < kMaxSlots; u++) {
+                v[u] = 0.0;
+                li[u] = kNo;
+                if (u < ns) {
                     v[u] = __ldcs(vp + 32 * u);
                     li[u] = __ldcs(ip + 32 * u);
                 }
-#pragma unroll
-                for (int u = 0; u < 4; u++) entry(v[u], li[u], xr, xs, acc, racc);
             }
-            for (; j < ns; j++, vp += 32, ip += 32) entry(__ldcs(vp), __ldcs(ip), xr, xs, acc, racc);
+            const double xr = rl != kNo ? xs[rl] : 0.0;
+            double racc = 0.0;
+#pragma unroll
+            for (int u = 0; u < kMaxSlots; u++) entry(v[u], li[u], xr, xs, acc, racc);
             if (rl != kNo) atomicAdd(&acc[rl], racc);
         }
         __syncthreads();
+        PHASE(2);
 
-        // 3. own rows: final up to later tiles' messages; store, then release
-        for (int r = m.r0 + tid; r < m.r1; r += kThreads) {
-            const int l = m.own_loff + (r - m.r0);
-            y[r] = fma(__ldg(P.diag + r), xs[l], acc[l]);
-        }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0 && m.r1 > m.r0) st_release(P.flags + t, epoch);
-
-        // 4. wait until the owners of every message target have stored
-        if (warp == 0) {
-            for (int w = m.w0 + lane; w < m.w1; w += 32) {
-                const int tl = __ldg(&P.wins[w].t_lo), th = __ldg(&P.wins[w].t_hi);
-                for (int u = tl; u <= th; u++)
-                    if (u != t)
-                        while (ld_acquire(P.flags + u) != epoch) {
-                        }
-            }
-        }
-        __syncthreads();
-
-        // 5. deliver the messages (slots outside the own rows)
-        if (nw <= 8) {
-            for (int w = m.w0; w < m.w1; w++) {
-                const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
-                          off = __ldg(&P.wins[w].loff);
-                for (int i = tid; i < len; i += kThreads) {
-                    const int c = lo + i;
-                    const double a = acc[off + i];
-                    if ((c < m.r0 || c >= m.r1) && a != 0.0) atomicAdd(y + c, a);
+        // 3. finish the slots; own rows add diag * x
+        if (m.u0 >= 0) {
+            const int32_t *uc = P.ucol + m.u0;
+            const int nmsg = m.local - nown;  // own rows are the tail of the list
+            if (P.accumulate) {
+                for (int i = tid; i < m.local; i += kThreads) {
+                    double a = acc[i];
+                    acc[i] = 0.0;
+                    if (i >= nmsg)
+                        a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + m.r0 + (i - nmsg)), xs[i], a);
+                    if (a != 0.0) atomicAdd(y + __ldg(uc + i), a);
                 }
+                __syncthreads();
+                continue;
+            }
+            for (int i = nmsg + tid; i < m.local; i += kThreads) {
+                y[m.r0 + (i - nmsg)] = fma(
+                    P.diag_const ? P.diag_alpha : __ldg(P.diag + m.r0 + (i - nmsg)), xs[i], acc[i]);
+                acc[i] = 0.0;
             }
         } else {
             for (int i = tid; i < m.local; i += kThreads) {
-                const int w = find_window(P.wins, m.w0, m.w1, i);
-                const int c = __ldg(&P.wins[w].lo) + (i - __ldg(&P.wins[w].loff));
-                const double a = acc[i];
-                if ((c < m.r0 || c >= m.r1) && a != 0.0) atomicAdd(y + c, a);
+                double a = acc[i];
+                acc[i] = 0.0;
+                const int r = m.r0 + (i - m.own_loff);
+                const bool own = i >= m.own_loff && i < m.own_loff + nown;
+                if (own) a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + r), xs[i], a);
+                if (own && !P.accumulate) y[r] = a;  // ordered: the owner stores first
+                xs[i] = (own && !P.accumulate) ? 0.0 : a;
+            }
+        }
+        if (!P.accumulate) {
+            __threadfence();
+            __syncthreads();
+            PHASE(3);
+            if (tid == 0) st_release(P.flags + t, epoch);
+            // 4. wait until the owners of every message target have stored
+            if (warp == 0) {
+                if (m.u0 >= 0) {
+                    for (int u = m.wt_lo + lane; u <= m.wt_hi; u += 32)
+                        if (u != t) wait_flag(P.flags, u, epoch, t, P.watchdog);
+                } else {
+                    for (int w = m.w0 + lane; w < m.w1; w += 32) {
+                        const int tl = __ldg(&P.wins[w].t_lo), th = __ldg(&P.wins[w].t_hi);
+                        for (int u = tl; u <= th; u++)
+                            if (u != t) wait_flag(P.flags, u, epoch, t, P.watchdog);
+                    }
+                }
             }
         }
         __syncthreads();
+        PHASE(4);
+
+        // 5. deliver: list mode by reductions, window mode by one bulk
+        //    reduction per window (odd-aligned windows by hand)
+        if (m.u0 >= 0) {
+            const int32_t *uc = P.ucol + m.u0;
+            const int nmsg = m.local - nown;
+            for (int i = tid; i < nmsg; i += kThreads) {
+                const double a = acc[i];
+                acc[i] = 0.0;
+                if (a != 0.0) atomicAdd(y + __ldg(uc + i), a);
+            }
+        } else {
+            if (tid == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                for (int w = m.w0; w < m.w1; w++) {
+                    const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
+                              off = __ldg(&P.wins[w].loff);
+                    if (tma_window(lo, len)) bulk_reduce_add(y + lo, xs + off, (uint32_t)len * 8);
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            for (int w = m.w0; w < m.w1; w++) {
+                const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
+                          off = __ldg(&P.wins[w].loff);
+                if (!tma_window(lo, len))
+                    for (int i = tid; i < len; i += kThreads)
+                        if (xs[off + i] != 0.0) atomicAdd(y + lo + i, xs[off + i]);
+            }
+            // xs is rewritten by the next tile: wait until the bulk reductions read it
+            if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncthreads();
+        PHASE(5);
     }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (P.phase_clk && tid == 0)
+        for (int k = 0; k < 6; k++) atomicAdd(P.phase_clk + k, (unsigned long long)clk[k]);
+#undef PHASE
 }
 
 __global__ void k_dot(int32_t n, const double *__restrict__ a, const double *__restrict__ b,
@@ -221,17 +400,21 @@ struct pars3_plan {
     size_t smem = 0;
     TileMeta *tiles = nullptr;
     Window *wins = nullptr;
-    int32_t *sbase = nullptr, *sns = nullptr;
-    uint16_t *srowl = nullptr;
-    double *val = nullptr;
-    uint16_t *lidx = nullptr;
+    int64_t *slice_off = nullptr;
+    uint8_t *rec = nullptr;
+    int32_t *ucol = nullptr;
+    int32_t stage_bytes = 0;
     double *diag = nullptr;
+    int32_t accumulate = 0, list_tiles = 0, watchdog = 0, diag_const = 0;
+    double diag_alpha = 0.0;
+    int32_t *trace_host = nullptr, *trace_dev = nullptr;
+    unsigned long long *phase_clk = nullptr;
     int32_t *flags = nullptr;
     int32_t *counter = nullptr;
     int64_t bytes = 0;
 
     ~pars3_plan() {
-        void *ptrs[] = {tiles, wins, sbase, sns, srowl, val, lidx, diag, flags, counter};
+        void *ptrs[] = {tiles, wins, slice_off, rec, ucol, diag, flags, counter};
         for (void *q : ptrs)
             if (q) cudaFree(q);
     }
@@ -252,7 +435,13 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         if (opt->local_slots > 0) o.local_slots = opt->local_slots;
         if (opt->seg_max > 0) o.seg_max = opt->seg_max;
         if (opt->gap >= 0) o.gap = opt->gap;
+        if (opt->mode > 0) o.mode = opt->mode;
     }
+    // the shared-memory budget (per-warp record rings + x/acc windows) caps both
+    if (o.seg_max > 8) o.seg_max = 8;
+    if (o.local_slots > 6144) o.local_slots = 6144;
+    o.max_segments = 32 * kMaxTileSlices;
+    if (o.seg_max > kMaxSlots) o.seg_max = kMaxSlots;
     HostPlan hp;
     int rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
                                     s->outer_row, s->outer_col, s->outer_val, o, hp);
@@ -263,12 +452,43 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     pl->beta = s->beta;
     pl->p = p;
     pl->ntiles = (int32_t)hp.tiles.size();
-    pl->nslices = (int32_t)hp.slice_base.size();
+    pl->nslices = (int32_t)hp.slice_off.size() - 1;
     pl->lmax = hp.max_local > 0 ? hp.max_local : 1;
+    pl->lmax = (pl->lmax + 1) & ~1;  // keep the accumulator array 16-byte aligned
     pl->nnz = hp.nnz;
-    pl->slots = (int64_t)hp.val.size();
+    pl->slots = hp.slots;
+    pl->stage_bytes = 64 + 320 * (hp.max_nslots > 0 ? hp.max_nslots : 1);
     pl->nwins = (int64_t)hp.wins.size();
+    pl->list_tiles = hp.list_tiles;
+    {
+        const char *wd = getenv("PARS3_WATCHDOG");
+        pl->watchdog = (wd && wd[0] == '1') ? 1 : 0;
+        const char *ph = getenv("PARS3_PHASES");
+        if (ph && ph[0] == '1') {
+            cudaMalloc((void **)&pl->phase_clk, 8 * sizeof(unsigned long long));
+            cudaMemset(pl->phase_clk, 0, 8 * sizeof(unsigned long long));
+        }
+        const char *tr = getenv("PARS3_TRACE");
+        if (tr && tr[0] == '1') {
+            if (cudaHostAlloc((void **)&pl->trace_host, 32 * 4096 * sizeof(int32_t),
+                              cudaHostAllocMapped) == cudaSuccess) {
+                memset(pl->trace_host, 0xff, 32 * 4096 * sizeof(int32_t));
+                cudaHostGetDevicePointer((void **)&pl->trace_dev, pl->trace_host, 0);
+            }
+        }
+    }
+    // accumulate mode (y zeroed, every contribution a reduction) when y is
+    // L2-sized or the matrix is unstructured; ordered mode (owner stores,
+    // later tiles reduce after the owner's flag) otherwise -- DESIGN.md
+    if (const char *md = getenv("PARS3_MODE")) o.mode = atoi(md);  // debug override
+    if (o.mode == 1) pl->accumulate = 0;
+    else if (o.mode == 2) pl->accumulate = 1;
+    else pl->accumulate = (s->n * 8 <= (64ll << 20)) || (4ll * hp.list_tiles > (int64_t)hp.tiles.size());
     std::vector<double> diag(s->diag, s->diag + s->n);
+    pl->diag_const = 1;
+    pl->diag_alpha = s->n ? diag[0] : 0.0;
+    for (int64_t i = 1; i < s->n && pl->diag_const; i++)
+        if (diag[i] != diag[0]) pl->diag_const = 0;
     std::vector<int32_t> zeros(pl->ntiles + 1, 0);
 #define UP(dst, src)                               \
     do {                                           \
@@ -281,11 +501,9 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     } while (0)
     UP(tiles, hp.tiles);
     UP(wins, hp.wins);
-    UP(sbase, hp.slice_base);
-    UP(sns, hp.slice_nslots);
-    UP(srowl, hp.slice_rowl);
-    UP(val, hp.val);
-    UP(lidx, hp.lidx);
+    UP(slice_off, hp.slice_off);
+    UP(rec, hp.rec);
+    UP(ucol, hp.ucol);
     UP(diag, diag);
     UP(flags, zeros);
 #undef UP
@@ -319,8 +537,10 @@ static int launch_tiles(pars3_plan *pl, const double *x, double *y, cudaStream_t
         CUDA_TRY(cudaMemsetAsync(pl->flags, 0, sizeof(int32_t) * pl->ntiles, st));
     }
     CUDA_TRY(cudaMemsetAsync(pl->counter, 0, sizeof(int32_t), st));
-    DevPlan P{pl->tiles, pl->wins, pl->sbase, pl->sns, pl->srowl, pl->val,
-              pl->lidx,  pl->diag, pl->flags, pl->counter, pl->ntiles, pl->lmax};
+    if (pl->accumulate) CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)pl->n, st));
+    DevPlan P{pl->tiles,   pl->wins,    pl->slice_off, pl->rec,  pl->ucol,        pl->diag,
+              pl->flags,   pl->counter, pl->ntiles,    pl->lmax, pl->stage_bytes, pl->accumulate,
+              pl->watchdog, pl->diag_const, pl->diag_alpha, pl->trace_dev, pl->phase_clk};
     k_tiles<<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
     LAUNCH_CHECK();
     return PARS3_OK;
@@ -367,6 +587,24 @@ extern "C" int pars3_plan_stats(const pars3_plan *pl, int64_t *stats) {
     stats[5] = pl->lmax;
     stats[6] = pl->grid;
     stats[7] = pl->bytes;
+    stats[8] = pl->list_tiles;
+    stats[9] = pl->accumulate;
+    return PARS3_OK;
+}
+
+// debug: per-phase cycle totals (PARS3_PHASES=1), summed over CTAs and launches
+extern "C" int pars3_plan_phases(const pars3_plan *pl, int64_t *out6) {
+    if (!pl || !out6) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
+    unsigned long long h[8] = {0};
+    if (pl->phase_clk) CUDA_TRY(cudaMemcpy(h, pl->phase_clk, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 6; k++) out6[k] = (int64_t)h[k];
+    return PARS3_OK;
+}
+
+// debug: host address of the trace buffer (PARS3_TRACE=1), else null
+extern "C" int pars3_plan_trace(const pars3_plan *pl, int32_t **host) {
+    if (!pl || !host) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
+    *host = pl->trace_host;
     return PARS3_OK;
 }
 

@@ -56,7 +56,7 @@ class Pars3Operator:
                               _lib.ptr(host["mid_col"]), _lib.ptr(host["mid_val"]),
                               int(host["outer_col"].size), _lib.ptr(host["outer_row"]),
                               _lib.ptr(host["outer_col"]), _lib.ptr(host["outer_val"]))
-        opts = _lib.PlanOptions(*(options or (0, 0, 0, -1)))
+        opts = _lib.PlanOptions(*(tuple(options or ()) + (0, 0, 0, -1, 0)[len(options or ()):]))
         bs = _c(block_start if block_start is not None else [0, self.n], np.int64)
         handle = ctypes.c_void_p()
         L = _lib.load()
@@ -101,10 +101,10 @@ class Pars3Operator:
         return int(b.value)
 
     def stats(self) -> dict:
-        a = np.zeros(8, dtype=np.int64)
+        a = np.zeros(10, dtype=np.int64)
         _lib.check(self._L.pars3_plan_stats(self._handle, _lib.ptr(a)))
         keys = ("tiles", "slices", "padded_slots", "entries", "windows", "max_local", "grid",
-                "device_bytes")
+                "device_bytes", "list_tiles", "accumulate")
         return {k: int(v) for k, v in zip(keys, a)}
 
     def close(self):

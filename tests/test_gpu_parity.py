@@ -132,10 +132,13 @@ def test_skew_identity_large():
 
 
 OPTION_SETS = [
-    (0, 0, 0, -1),        # defaults
-    (64, 128, 8, 0),      # tiny tiles: forces splits, many windows, hub chunks
-    (32, 64, 4, 2),       # smallest local space: every wide row is chunked
-    (4096, 65535, 64, 64),
+    (0, 0, 0, -1, 0),         # defaults (auto mode)
+    (0, 0, 0, -1, 1),         # ordered mode forced (owner stores + flags)
+    (0, 0, 0, -1, 2),         # accumulate mode forced
+    (64, 128, 8, 0, 1),       # tiny tiles: splits, list-mode tiles, hub chunks; ordered
+    (64, 128, 8, 0, 2),
+    (32, 64, 4, 2, 1),        # smallest local space: every wide row is chunked
+    (4096, 65535, 64, 64, 1),   # clamped to the shared-memory budget
 ]
 
 
