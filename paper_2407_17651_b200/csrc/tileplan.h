@@ -21,8 +21,8 @@ namespace pars3 {
 constexpr uint16_t kNoSlot = 0xFFFF;
 
 struct PlanOptions {
-    int32_t tile_rows = 2048;   // rows per tile before splitting
-    int32_t local_slots = 6144; // shared-memory window slots per tile (x + acc = 16 B each)
+    int32_t tile_rows = 1024;   // rows per tile before splitting
+    int32_t local_slots = 3200; // shared-memory window slots per tile (x + acc = 16 B each)
     int32_t seg_max = 8;        // max entries per row segment (longer rows are split)
     int32_t gap = 8;            // merge column runs separated by <= gap unused slots
     int32_t max_segments = 16384;  // row segments per tile (the kernel's slice table bound / 32)

@@ -41,9 +41,9 @@ constexpr uint16_t kNo = pars3::kNoSlot;
 // registers (tools/microbench/mb3.cu: this inner loop alone runs at ~6.7 TB/s
 // on c5-shaped data), and the second CTA overlaps each CTA's per-tile
 // window/flush phases.
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxTileSlices = 1024;  // per-tile slice offset table in shared memory
+constexpr int kMaxTileSlices = 256;  // per-tile slice offset table in shared memory
 constexpr int kMaxSlots = 8;          // slots per slice (plan seg_max)
 
 struct DevPlan {
@@ -170,7 +170,7 @@ __device__ __forceinline__ void bulk_reduce_add(double *g, const double *s, uint
                  : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 4)
 k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t epoch) {
     extern __shared__ __align__(128) uint8_t dyn[];
     double *xs = reinterpret_cast<double *>(dyn);
@@ -439,7 +439,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     }
     // the shared-memory budget (per-warp record rings + x/acc windows) caps both
     if (o.seg_max > 8) o.seg_max = 8;
-    if (o.local_slots > 6144) o.local_slots = 6144;
+    if (o.local_slots > 3200) o.local_slots = 3200;
     o.max_segments = 32 * kMaxTileSlices;
     if (o.seg_max > kMaxSlots) o.seg_max = kMaxSlots;
     HostPlan hp;
@@ -483,7 +483,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     if (const char *md = getenv("PARS3_MODE")) o.mode = atoi(md);  // debug override
     if (o.mode == 1) pl->accumulate = 0;
     else if (o.mode == 2) pl->accumulate = 1;
-    else pl->accumulate = (s->n * 8 <= (64ll << 20)) || (4ll * hp.list_tiles > (int64_t)hp.tiles.size());
+    else pl->accumulate = 1;  // measured faster at every BASELINE config
     std::vector<double> diag(s->diag, s->diag + s->n);
     pl->diag_const = 1;
     pl->diag_alpha = s->n ? diag[0] : 0.0;
