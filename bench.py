@@ -223,86 +223,141 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PARS3_DIST_BACKEND", "nccl")  # gloo: test the N>1 path on 1 GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     m, s, bw, beta, x_host = build_problem(args.config, args.beta)
     n, nnz = m.n, m.nnz_offdiag
-    plan, _ = P.classify_conflicts(s, P.partition_rows(n, 1))
+    plan, _ = P.classify_conflicts(s, P.partition_rows(n, world))
+    lo, hi = int(plan.block_start[rank]), int(plan.block_start[rank + 1])
     t0 = time.time()
-    op = P.prepare(s, plan)
+    if world == 1:
+        op = P.prepare(s, plan)
+        launches_per_step = op.kernel_count(with_dot=True)
+        stats = op.stats()
+    else:
+        from paper_2407_17651_b200.distributed import DistributedPars3
+        dop = DistributedPars3(s, plan)
+        op = dop._op
+        launches_per_step = op.kernel_count(with_dot=False) + 1
+        stats = op.stats()
     torch.cuda.synchronize()
-    log(f"upload + device plan {time.time() - t0:.1f}s, plan bytes {op.plan_bytes()}")
-    x = torch.from_numpy(x_host).cuda()
-    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    log(f"rank {rank}: rows [{lo}, {hi}) device plan {time.time() - t0:.1f}s {stats}")
+    x = torch.from_numpy(x_host[lo:hi].copy()).cuda()
     dot = torch.zeros(1, dtype=torch.float64, device="cuda")
 
-    # parity check of this run's product against the oracle (outside the clock)
-    op.matvec(x, y)
+    def step():
+        """One MRS-style step: y = A x and <y, y> (reduced over ranks)."""
+        if dist is None:
+            y, d = op.matvec_dot(x, None, y=ybuf, dot=dot)
+            return y
+        y = dop.matvec(x)
+        d = torch.dot(y, y).reshape(1)
+        dist.all_reduce(d)
+        return y
+
+    ybuf = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+    y = step()
     torch.cuda.synchronize()
-    y_ref = O.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x_host) \
-        if rank == 0 and not args.no_check else None
-    parity = O.rel_err(y.cpu().numpy(), y_ref) if y_ref is not None else None
-    log(f"parity rel_err vs oracle serial: {parity}")
+    # parity of this run's product against the oracle (outside the clock)
+    parity = None
+    if not args.no_check:
+        yb = y.cpu().numpy()
+        if dist is not None:
+            sizes = np.diff(plan.block_start)
+            width = int(sizes.max())
+            pad = torch.zeros(width, dtype=torch.float64, device="cuda")
+            pad[:hi - lo] = y
+            parts = [torch.zeros(width, dtype=torch.float64, device="cuda") for _ in range(world)]
+            dist.all_gather(parts, pad)
+            yb = np.concatenate([parts[r][:int(sizes[r])].cpu().numpy() for r in range(world)])
+        if rank == 0:
+            y_ref = O.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x_host)
+            parity = O.rel_err(yb, y_ref)
+            log(f"parity rel_err vs oracle serial: {parity}")
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up
+    def max_over_ranks(ms):
+        if dist is None:
+            return ms
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     for _ in range(args.warmup):
-        op.matvec_dot(x, y, y, dot)
+        step()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record()
         for _ in range(args.steps):
-            op.matvec_dot(x, y, y, dot)
+            step()
         ev1.record()
         barrier()
-    step_ms = ev0.elapsed_time(ev1) / args.steps
-    if dist is not None:
-        t = torch.tensor([step_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms = float(t.item())
+    step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
 
-    # dominant kernel: the SpMV alone, same clock discipline
+    # dominant kernel: the local SpMV alone, same clock discipline
+    xk = dop.x_ext if dist is not None else x
+    yk = dop.y_ext if dist is not None else ybuf
     barrier()
     ev0.record()
     for _ in range(args.steps):
-        op.matvec(x, y)
+        op.matvec(xk, yk)
     ev1.record()
     barrier()
-    spmv_ms = ev0.elapsed_time(ev1) / args.steps
+    spmv_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
 
     # end to end through the public API: pinned host x in, host y out
-    x_pin = torch.from_numpy(x_host).pin_memory()
-    y_pin = torch.empty(n, dtype=torch.float64).pin_memory()
-    P.spmv_pars3(s, plan, x_pin, out=y_pin)
+    x_pin = torch.from_numpy(x_host[lo:hi].copy()).pin_memory()
+    y_pin = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        if dist is None:
+            P.spmv_pars3(s, plan, x_pin if world == 1 else None, out=y_pin)
+            return
+        xd = x_pin.to("cuda", non_blocking=True)
+        y_pin.copy_(dop.matvec(xd), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    if world == 1:
+        x_pin = torch.from_numpy(x_host).pin_memory()
+        y_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+    e2e_step()
     barrier()
     t_e = time.perf_counter()
     ev0.record()
     for _ in range(args.steps):
-        P.spmv_pars3(s, plan, x_pin, out=y_pin)
+        e2e_step()
     ev1.record()
     barrier()
-    e2e_ms = ev0.elapsed_time(ev1) / args.steps
+    e2e_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     e2e_wall_ms = (time.perf_counter() - t_e) * 1e3 / args.steps
 
     B = algorithmic_bytes(n, nnz)
     F = algorithmic_flops(n, nnz)
     peak, peak_src = peak_hbm()
-    value = world * B / (step_ms * 1e-3) / 1e9
-    achieved = B / (spmv_ms * 1e-3) / 1e9
+    value = B / (step_ms * 1e-3) / 1e9
+    # per-GPU kernel roofline: this rank's share of the algorithmic bytes
+    own_nnz = int(stats["entries"])
+    B_rank = algorithmic_bytes(hi - lo, own_nnz) if world > 1 else B
+    achieved = B_rank / (spmv_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.config)
+            traffic = json.load(open(tpath)).get(args.config) if world == 1 else None
         except Exception:
             traffic = None
     if rank != 0:
@@ -315,24 +370,29 @@ def run_gpu(args):
     out = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, BASELINE config; random-init values U(-1,1))",
         "config": {"workload": args.config, "n": n, "nnz_lower": nnz, "beta": beta,
                    "rcm_bandwidth": bw, "step": "y = A x fused with <y, y>",
                    "bytes_per_spmv": B, "flops_per_spmv": F,
                    "l2": "inputs larger than L2 (matrix stream 3.07 GB per step)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
-        "gflops": world * F / (step_ms * 1e-3) / 1e9,
+                   "parallelism": (f"row blocks x{world} (partition_rows), NCCL halo + "
+                                   "accumulation exchange" if world > 1 else "single GPU")},
+        "gflops": F / (step_ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel_ms": spmv_ms, "frac_of_8TBs": achieved / 8000.0},
+                     "kernel_ms": spmv_ms, "frac_of_8TBs": achieved / 8000.0,
+                     "bytes_per_launch": B_rank},
         "cpu_baseline": cpu,
-        "e2e": {"value": B / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
-                "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms, "wall_ms_per_step": e2e_wall_ms,
-                "api": "spmv_pars3(s, plan, x_pinned_host_tensor, out=y_pinned_host_tensor)"},
-        "gpu_launches": args.steps * op.kernel_count(with_dot=True),
+        "e2e": {"value": B / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms,
+                "wall_ms_per_step": e2e_wall_ms,
+                "api": ("spmv_pars3(s, plan, x_pinned_host_tensor, out=y_pinned_host_tensor)"
+                        if world == 1 else "DistributedPars3.matvec on pinned host blocks")},
+        "gpu_launches": args.steps * launches_per_step,
         "clocks": clk.summary(),
         "parity_rel_err": parity,
+        "plan": stats,
     }
     print(json.dumps(out), flush=True)
     if dist is not None:

@@ -512,8 +512,10 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         PARS3_FAIL(PARS3_ERR_CUDA, "cudaMalloc failed");
     }
     pl->smem = sizeof(double) * 2 * (size_t)pl->lmax;
+    // the attribute is per function, shared by every plan: set it to the
+    // largest window space any plan may use, not to this plan's size
     cudaError_t e = cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)pl->smem);
+                                         (int)(sizeof(double) * 2 * 3200));
     int per_sm = 0, sms = 0, dev = 0;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -1,0 +1,268 @@
+"""Row-block sharding of the PARS3 product across ranks (one GPU per rank).
+
+The reference runs its workers as threads over one shared x and y and keeps
+the paper's MPI protocol only as a simulation (parallel.py:274-413,
+PAPER.md:151, 197).  Here each rank owns the rows ``[lo, hi)`` of the
+reference's own partition (``partition_rows(n, p)``, split.py:173-188) -- their
+diagonal, middle and outer entries -- and one product is one exchange step:
+
+1. **x halo** (predecessors -> successor): rank w receives
+   ``x[halo_lo_w, lo_w)``, the columns below its block that its rows read.
+   This is the paper's staged X chain, in the lower-storage direction
+   (SPEC.md D16).
+2. **local product** over the rank's extended index space
+   ``[halo_lo_w, hi_w)``: own rows carry their entries, halo rows none, so
+   ``y_ext`` holds the own rows' values and, in its halo part, the mirrors
+   ``-a_ic * x_i`` bound for earlier blocks.
+3. **accumulation** (successor -> predecessors): the halo part of ``y_ext``
+   travels back and the owner adds it -- the reference's accumulation
+   messages / ``MPI_Accumulate`` (parallel.py:96-113), as dense segments.
+
+The halo here spans middle and outer entries (the reference's
+``PartitionPlan.halo_lo`` covers the middle band only, split.py:341-345,
+because its outer pass runs on worker 0).  The reference's
+plan arrays are not altered.
+
+Communication uses ``torch.distributed`` point-to-point ops
+(``batch_isend_irecv``): NCCL over NVLink with device tensors, or gloo with
+host staging for CPU tests.  The local product is the GPU tile kernel; tests
+may inject another local product (``local_factory``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .split import BandSplit, PartitionPlan
+
+__all__ = ["RankShard", "shard_for_rank", "exchange_schedule", "DistributedPars3"]
+
+
+@dataclass
+class RankShard:
+    """Rank w's rows in its extended index space ``[halo_lo, hi)``."""
+
+    rank: int
+    lo: int
+    hi: int
+    halo_lo: int
+    # SSS arrays over n_ext = hi - halo_lo rows (halo rows empty)
+    row_ptr: np.ndarray
+    col_ind: np.ndarray
+    off_diags: np.ndarray
+    diags: np.ndarray
+
+    @property
+    def n_ext(self) -> int:
+        return self.hi - self.halo_lo
+
+    @property
+    def own_off(self) -> int:
+        return self.lo - self.halo_lo
+
+
+def _rows_entries(s: BandSplit, lo: int, hi: int):
+    """Merged (outer then middle) columns/values of rows [lo, hi), per row
+    ascending, plus the per-row counts (the merge_splits order, split.py:144-170)."""
+    orow = s.outer_row
+    o0, o1 = np.searchsorted(orow, [lo, hi])
+    ocount = np.bincount(orow[o0:o1] - lo, minlength=hi - lo)
+    m0, m1 = int(s.mid_ptr[lo]), int(s.mid_ptr[hi])
+    mcount = np.diff(s.mid_ptr[lo:hi + 1])
+    rp = np.zeros(hi - lo + 1, dtype=np.int64)
+    np.cumsum(ocount + mcount, out=rp[1:])
+    col = np.empty(int(rp[-1]), dtype=np.int64)
+    val = np.empty(int(rp[-1]), dtype=np.float64)
+    optr = np.zeros(hi - lo + 1, dtype=np.int64)
+    np.cumsum(ocount, out=optr[1:])
+    rows_o = np.repeat(np.arange(hi - lo), ocount)
+    dest_o = rp[rows_o] + (np.arange(o1 - o0) - optr[rows_o])
+    rows_m = np.repeat(np.arange(hi - lo), mcount)
+    dest_m = rp[rows_m] + ocount[rows_m] + (np.arange(m1 - m0) - (s.mid_ptr[lo:hi][rows_m] - m0))
+    col[dest_o] = s.outer_col[o0:o1]
+    val[dest_o] = s.outer_val[o0:o1]
+    col[dest_m] = s.mid_col[m0:m1]
+    val[dest_m] = s.mid_val[m0:m1]
+    return rp, col, val
+
+
+def shard_for_rank(s: BandSplit, plan: PartitionPlan, rank: int) -> RankShard:
+    lo, hi = int(plan.block_start[rank]), int(plan.block_start[rank + 1])
+    rp, col, val = _rows_entries(s, lo, hi)
+    halo_lo = int(min(lo, col.min())) if col.size else lo
+    own_off = lo - halo_lo
+    n_ext = hi - halo_lo
+    row_ptr = np.zeros(n_ext + 1, dtype=np.int64)
+    row_ptr[own_off:] = rp
+    diags = np.zeros(n_ext)
+    diags[own_off:] = s.diag[lo:hi]
+    return RankShard(rank, lo, hi, halo_lo, row_ptr, (col - halo_lo).astype(np.int32), val, diags)
+
+
+def exchange_schedule(s: BandSplit, plan: PartitionPlan):
+    """Every rank's halo range, and the (src, dst, a, b) segments: rank dst
+    needs x[a, b) from owner src (and returns y partials for the same range)."""
+    p = plan.p
+    halos = []
+    for w in range(p):
+        lo, hi = int(plan.block_start[w]), int(plan.block_start[w + 1])
+        m0, m1 = int(s.mid_ptr[lo]), int(s.mid_ptr[hi])
+        cmin = lo
+        if m1 > m0:
+            cmin = min(cmin, int(s.mid_col[m0:m1].min()))
+        o0, o1 = np.searchsorted(s.outer_row, [lo, hi])
+        if o1 > o0:
+            cmin = min(cmin, int(s.outer_col[o0:o1].min()))
+        halos.append(cmin)
+    segs = []
+    bs = plan.block_start
+    for dst in range(p):
+        a0, b0 = halos[dst], int(bs[dst])
+        for src in range(dst):
+            a, b = max(a0, int(bs[src])), min(b0, int(bs[src + 1]))
+            if a < b:
+                segs.append((src, dst, a, b))
+    return halos, segs
+
+
+class DistributedPars3:
+    """One rank's operator: ``y_own = (A x)[lo:hi]`` from ``x_own = x[lo:hi]``.
+
+    ``plan.p`` must equal the world size; rank r owns block r.  With
+    ``local_factory`` (tests) the local product is ``local_factory(shard)``
+    returning a callable ``y_ext = f(x_ext)`` on host arrays; otherwise the
+    GPU tile kernel runs it on the rank's device.
+    """
+
+    def __init__(self, s: BandSplit, plan: PartitionPlan, group=None, local_factory=None,
+                 device=None, options=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        if plan.p != world:
+            raise ValueError(f"plan has {plan.p} blocks but the group has {world} ranks")
+        if plan.n != s.n or plan.beta != s.beta:
+            raise ValueError(f"plan (n={plan.n}, beta={plan.beta}) does not match "
+                             f"split (n={s.n}, beta={s.beta})")
+        self.shard = shard_for_rank(s, plan, self.rank)
+        self.halos, self.segs = exchange_schedule(s, plan)
+        assert self.halos[self.rank] == self.shard.halo_lo
+        self.staged = dist.get_backend(group) == "gloo"
+        sh = self.shard
+        if local_factory is not None:
+            self._local = local_factory(sh)
+            self.device = torch.device("cpu")
+            self._on_host = True
+        else:
+            from .device import Pars3Operator
+            self.device = torch.device(device) if device is not None else torch.device(
+                "cuda", torch.cuda.current_device())
+            e = np.zeros(0, np.int32)
+            self._op = Pars3Operator(sh.n_ext, max(1, sh.n_ext), sh.diags, sh.row_ptr, sh.col_ind,
+                                     sh.off_diags, e, e, np.zeros(0), device=self.device,
+                                     options=options)
+            self._on_host = False
+        t = torch.float64
+        self.x_ext = torch.zeros(sh.n_ext, dtype=t, device=self.device)
+        self.y_ext = torch.zeros(sh.n_ext, dtype=t, device=self.device)
+        self._inbox = {(dst, a): torch.empty(b - a, dtype=t, device=self.device)
+                       for (src, dst, a, b) in self.segs if src == self.rank}
+
+    # -- communication --------------------------------------------------
+    def _p2p(self, ops):
+        if not ops:
+            return
+        dist = self.dist
+        if self.staged and not self._on_host:
+            # gloo moves host tensors: stage device buffers through the host
+            host_ops, copies = [], []
+            for kind, tensor, peer in ops:
+                h = tensor.detach().cpu()
+                host_ops.append((kind, h, peer))
+                copies.append((tensor, h, kind))
+            reqs = dist.batch_isend_irecv([dist.P2POp(k, h, peer, self.group)
+                                           for k, h, peer in host_ops])
+            for r in reqs:
+                r.wait()
+            for tensor, h, kind in copies:
+                if kind is dist.irecv:
+                    tensor.copy_(h)
+            return
+        reqs = dist.batch_isend_irecv([dist.P2POp(k, tns, peer, self.group)
+                                       for k, tns, peer in ops])
+        for r in reqs:
+            r.wait()
+
+    def _peer(self, r):
+        return self.dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def matvec(self, x_own):
+        """y_own for this rank's block; x_own: length hi - lo (this rank's x)."""
+        sh, dist = self.shard, self.dist
+        nown = sh.hi - sh.lo
+        if x_own.shape[0] != nown:
+            raise ValueError(f"x block must have {nown} entries, got {x_own.shape[0]}")
+        self.x_ext[sh.own_off:] = x_own.to(self.device)
+        # 1. x halo: owners send slices of their block, consumers receive
+        ops = []
+        for (src, dst, a, b) in self.segs:
+            if src == self.rank:
+                ops.append((dist.isend, self.x_ext[sh.own_off + (a - sh.lo):
+                                                   sh.own_off + (b - sh.lo)].contiguous(),
+                            self._peer(dst)))
+            elif dst == self.rank:
+                ops.append((dist.irecv, self.x_ext[a - sh.halo_lo:b - sh.halo_lo], self._peer(src)))
+        self._p2p(ops)
+        # 2. local product over [halo_lo, hi)
+        if self._on_host:
+            self.y_ext.copy_(self.torch.from_numpy(np.asarray(self._local(self.x_ext.numpy()))))
+        else:
+            self._op.matvec(self.x_ext, self.y_ext)
+        # 3. accumulation messages back to the owners, added in source order
+        ops = []
+        for (src, dst, a, b) in self.segs:
+            if dst == self.rank:
+                ops.append((dist.isend, self.y_ext[a - sh.halo_lo:b - sh.halo_lo].contiguous(),
+                            self._peer(src)))
+            elif src == self.rank:
+                ops.append((dist.irecv, self._inbox[(dst, a)], self._peer(dst)))
+        self._p2p(ops)
+        y_own = self.y_ext[sh.own_off:].clone()
+        for (src, dst, a, b) in self.segs:
+            if src == self.rank:
+                y_own[a - sh.lo:b - sh.lo] += self._inbox[(dst, a)]
+        return y_own
+
+
+def emulate_ranks(s: BandSplit, plan: PartitionPlan, x, make_local):
+    """Run the p-rank protocol sequentially in one process: the same shards,
+    schedule and data movement as DistributedPars3, with the exchanges as
+    direct copies.  ``make_local(shard)`` returns ``y_ext = f(x_ext)`` (for
+    the GPU path: a tile-kernel operator on the rank's extended space).
+    Returns y as a torch tensor on ``x``'s device."""
+    import torch
+    p = plan.p
+    shards = [shard_for_rank(s, plan, w) for w in range(p)]
+    halos, segs = exchange_schedule(s, plan)
+    local = [make_local(sh) for sh in shards]
+    x = torch.as_tensor(x, dtype=torch.float64)
+    x_ext = []
+    for sh in shards:
+        xe = torch.zeros(sh.n_ext, dtype=torch.float64, device=x.device)
+        xe[sh.own_off:] = x[sh.lo:sh.hi]
+        x_ext.append(xe)
+    for (src, dst, a, b) in segs:  # 1. x halo
+        sd, ss = shards[dst], shards[src]
+        x_ext[dst][a - sd.halo_lo:b - sd.halo_lo] = x_ext[src][ss.own_off + (a - ss.lo):
+                                                               ss.own_off + (b - ss.lo)]
+    y_ext = [local[w](x_ext[w]) for w in range(p)]  # 2. local products
+    y = torch.cat([y_ext[w][shards[w].own_off:] for w in range(p)])
+    for (src, dst, a, b) in segs:  # 3. accumulation, in the same order as the ranks
+        sd = shards[dst]
+        y[a:b] += y_ext[dst][a - sd.halo_lo:b - sd.halo_lo]
+    return y

@@ -76,6 +76,18 @@ def _from_pairs(n, r, c, relabel_seed, val_seed, values="uniform", alpha=0.0, na
     return LowerSss(n, row_ptr, cols, val, np.full(n, float(alpha)), name)
 
 
+def _sorted_unique(key: np.ndarray) -> np.ndarray:
+    """np.unique for large int64 keys via an in-place sort (np.unique's hash
+    path is several times slower at 10^8 keys); same result."""
+    key.sort()
+    if key.size < 2:
+        return key
+    keep = np.empty(key.size, dtype=bool)
+    keep[0] = True
+    np.not_equal(key[1:], key[:-1], out=keep[1:])
+    return key[keep]
+
+
 def _grid_pairs(k, dims, stencil):
     """Lower neighbour pairs (i, j) with j < i of a k^dims grid, natural ids."""
     n = k ** dims
@@ -210,7 +222,7 @@ def random_band(n, half_width=2048, per_row=16, far_frac=0.01, seed_struct=0, se
     if n_far and n > half_width + 1:
         fr = rng.integers(half_width + 1, n, size=n_far)
         fc = (rng.random(n_far) * (fr - half_width)).astype(np.int64)
-        key = np.unique(fr * n + fc)
+        key = _sorted_unique(fr * n + fc)
         fr, fc = key // n, key % n
         r_band = np.concatenate((r_band, fr))
         c_band = np.concatenate((c_band, fc))
@@ -225,20 +237,30 @@ def rmat(scale, edge_factor=16, abcd=(0.57, 0.19, 0.19, 0.05), seed_struct=0, se
     e = edge_factor * n
     a, b, c, _ = abcd
     rng = np.random.default_rng(seed_struct)
-    src = np.zeros(e, dtype=np.int64)
-    dst = np.zeros(e, dtype=np.int64)
+    src = np.zeros(e, dtype=np.int32)
+    dst = np.zeros(e, dtype=np.int32)
+    ge_a = np.empty(e, dtype=bool)
+    ge_ab = np.empty(e, dtype=bool)
+    ge_abc = np.empty(e, dtype=bool)
     for bit in range(scale):
         u = rng.random(e)
-        sbit = u >= a + b
-        dbit = ((u >= a) & (u < a + b)) | (u >= a + b + c)
-        src |= sbit.astype(np.int64) << bit
-        dst |= dbit.astype(np.int64) << bit
+        np.greater_equal(u, a, out=ge_a)
+        np.greater_equal(u, a + b, out=ge_ab)
+        np.greater_equal(u, a + b + c, out=ge_abc)
+        del u
+        # source bit: quadrant c or d; destination bit: quadrant b or d
+        src |= ge_ab.view(np.int8).astype(np.int32) << bit
+        np.logical_xor(ge_a, ge_ab, out=ge_a)
+        np.logical_or(ge_a, ge_abc, out=ge_a)
+        dst |= ge_a.view(np.int8).astype(np.int32) << bit
+    src = src.astype(np.int64)
+    dst = dst.astype(np.int64)
     keep = src != dst
     src, dst = src[keep], dst[keep]
     lo_r = np.maximum(src, dst)
     lo_c = np.minimum(src, dst)
     del src, dst
-    key = np.unique(lo_r * n + lo_c)
+    key = _sorted_unique(lo_r * n + lo_c)
     r, cc = key // n, key % n
     return _from_pairs(n, r, cc, seed_perm, seed_val, values="normal", name=name)
 

@@ -174,3 +174,27 @@ def test_spmv_dot(oracle):
     y, dot = op.matvec_dot(x, None)
     yh = y.cpu().numpy()
     assert abs(float(dot.item()) - float(yh @ yh)) <= 1e-12 * float(yh @ yh)
+
+
+@pytest.mark.parametrize("p", [2, 3, 8])
+def test_multirank_protocol_on_one_gpu(p, oracle):
+    """The p-rank sharding with the GPU tile kernel as each rank's local
+    product, exchanges emulated in-process (one GPU is available)."""
+    import torch
+    from paper_2407_17651_b200 import generators as G
+    from paper_2407_17651_b200.device import Pars3Operator
+    from paper_2407_17651_b200.distributed import emulate_ranks
+    for g, beta in ((G.stencil27(40, seed_val=4, alpha=0.5), None),
+                    (G.random_band(40000, 300, 8, 0.01, seed_struct=1, seed_perm=2, seed_val=3), 16)):
+        m, s, plan = _pipeline(g, beta=beta, p=p)
+        x = G.make_x(m.n, 11)
+
+        def make_local(sh):
+            e = np.zeros(0, np.int32)
+            op = Pars3Operator(sh.n_ext, max(1, sh.n_ext), sh.diags, sh.row_ptr, sh.col_ind,
+                               sh.off_diags, e, e, np.zeros(0))
+            return lambda xe: op.matvec(xe)
+
+        y = emulate_ranks(s, plan, torch.from_numpy(x).cuda(), make_local).cpu().numpy()
+        y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x)
+        assert rel_err(y, y_ref) <= TOL, (g.name, p)

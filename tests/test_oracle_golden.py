@@ -87,31 +87,3 @@ def test_c1_full_chain_bit_exact(oracle, golden_c1):
             for f in PLAN_FIELDS:
                 assert np.array_equal(plan[f], z[f"b{b}/p{p}/{f}"]), (b, p, f)
             assert np.array_equal(oracle.spmv_pars3(s, plan, x), z[f"b{b}/p{p}/y_pars3"])
-
-
-@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
-def test_config_chain_hashes(oracle, golden_hashes, cfg):
-    """The oracle chain reproduces the reference chain's SHA-256s (c3/c4 are
-    present only when make_golden.py ran with --big)."""
-    if cfg not in golden_hashes:
-        pytest.skip(f"{cfg} hashes not generated")
-    from paper_2407_17651_b200 import generators as G
-    h = golden_hashes[cfg]
-    g = G.make_config(cfg)
-    ip, ix = oracle.pattern_from_sss(g.n, g.row_ptr, g.col_ind)
-    fw = oracle.rcm_order(g.n, ip, ix)
-    assert sha(fw) == h["rcm_forward"]
-    rp, ci, od, dg = oracle.permute_sss(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags, fw)
-    for a, k in ((rp, "row_ptr"), (ci, "col_ind"), (od, "off_diags"), (dg, "diags")):
-        assert sha(a) == h[k], k
-    x = G.make_x(g.n, G.CONFIGS[cfg]["seed_x"])
-    assert sha(x) == h["x"]
-    assert sha(oracle.spmv_serial(rp, ci, od, dg, x)) == h["y_serial"]
-    beta = int(h["beta"])
-    s = oracle.split_bands(g.n, rp, ci, od, dg, beta)
-    for f in SPLIT_FIELDS:
-        assert sha(s[f]) == h[f"b{beta}/{f}"], f
-    plan = oracle.classify_conflicts(s, oracle.partition_rows(g.n, 8))
-    for f in PLAN_FIELDS:
-        assert sha(plan[f]) == h[f"b{beta}/p8/{f}"], f
-    assert sha(oracle.spmv_pars3(s, plan, x)) == h[f"b{beta}/p8/y_pars3"]

@@ -66,29 +66,6 @@ def test_c1_chain(lib_built, golden_c1):
                 assert np.array_equal(getattr(plan, f), z[f"b{b}/p{p}/{f}"]), (b, p, f)
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
-def test_config_chain_hashes(lib_built, golden_hashes, cfg):
-    if cfg not in golden_hashes:
-        pytest.skip(f"{cfg} hashes not generated")
-    from paper_2407_17651_b200 import generators as G
-    h = golden_hashes[cfg]
-    g = G.make_config(cfg)
-    m0 = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
-    perm = P.rcm_order(P.pattern_from_sss(m0))
-    assert sha(perm.forward) == h["rcm_forward"]
-    m = P.permute_sss(m0, perm)
-    for k in ("row_ptr", "col_ind", "off_diags", "diags"):
-        assert sha(getattr(m, k)) == h[k], k
-    beta = int(h["beta"])
-    assert P.default_beta(m.n, P.compute_bandwidth(m)) == beta
-    s = P.split_bands(m, beta)
-    for f in SPLIT_FIELDS:
-        assert sha(getattr(s, f)) == h[f"b{beta}/{f}"], f
-    plan, _ = P.classify_conflicts(s, P.partition_rows(m.n, 8))
-    for f in PLAN_FIELDS:
-        assert sha(getattr(plan, f)) == h[f"b{beta}/p8/{f}"], f
-
-
 def test_rcm_disconnected_and_isolated(lib_built, oracle):
     """Several components + isolated nodes (D8/D9) against the oracle."""
     from paper_2407_17651_b200 import generators as G
