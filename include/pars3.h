@@ -70,12 +70,12 @@ typedef struct pars3_split_view {
 
 /* Tiling knobs of the device plan; 0 (or NULL options) = default. */
 typedef struct pars3_plan_options {
-    int32_t tile_rows;    /* rows per tile before splitting (2048) */
-    int32_t local_slots;  /* shared-memory window slots per tile (6144) */
-    int32_t seg_max;      /* max entries per row segment (64) */
+    int32_t tile_rows;    /* rows per tile before splitting (1024) */
+    int32_t local_slots;  /* shared-memory window slots per tile (<= 3200 fp64 / 2496 fixed) */
+    int32_t seg_max;      /* max entries per row segment (<= 8) */
     int32_t gap;          /* merge column runs separated by <= gap slots (8); -1 = default */
-    int32_t mode;         /* 0 auto, 1 ordered (owners store, later tiles reduce after the
-                             owner's flag), 2 accumulate (y zeroed, all contributions reduce) */
+    int32_t mode;         /* accumulation of the mirror sums: 0 auto, 1 exact-integer fixed
+                             point (3 x 32-bit words), 2 fp64 shared-memory atomics */
 } pars3_plan_options;
 
 /* Build the device plan of a split on the current device: replaces the

@@ -5,6 +5,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <new>
 
@@ -50,6 +51,7 @@ struct Built {               // one draft materialised
     std::vector<uint8_t> rec;
     int32_t r0, r1, local, own_loff, max_nslots = 0;
     int64_t nnz, slots;
+    double vmax = 0.0;
 };
 
 // Merge sorted unique columns into dense windows (runs separated by <= gap
@@ -203,6 +205,7 @@ void materialise(const Rows &R, const Draft &d, const PlanOptions &o, Built &b) 
             for (int64_t k = sg.kb; k < sg.ke; k++) {
                 const size_t pos = (size_t)(k - sg.kb) * 32 + l;
                 val[pos] = R.val(sg.row, k);
+                b.vmax = std::max(b.vmax, std::fabs(val[pos]));
                 lidx[pos] = (uint16_t)local_of(d, b.wloff, R.col(sg.row, k));
                 b.nnz++;
             }
@@ -299,7 +302,11 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
             m.u0 = b.list ? (int32_t)u_off[t] : -1;
             m.wt_lo = INT32_MAX;
             m.wt_hi = -1;
-            m.pad = 0;
+            {
+                int e = -1074;
+                if (b.vmax > 0.0) std::frexp(b.vmax, &e);  // vmax < 2^e
+                m.ev = e;
+            }
             if (b.list) {
                 std::memcpy(&P.ucol[u_off[t]], b.ucol.data(), b.ucol.size() * sizeof(int32_t));
                 for (size_t w = 0; w < b.wlo.size(); w++) {

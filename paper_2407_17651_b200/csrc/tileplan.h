@@ -26,7 +26,7 @@ struct PlanOptions {
     int32_t seg_max = 8;        // max entries per row segment (longer rows are split)
     int32_t gap = 8;            // merge column runs separated by <= gap unused slots
     int32_t max_segments = 16384;  // row segments per tile (the kernel's slice table bound / 32)
-    int32_t mode = 0;           // 0 auto, 1 ordered (owner stores + flags), 2 accumulate (y zeroed, all reductions)
+    int32_t mode = 0;           // accumulation: 0 auto, 1 fixed point, 2 fp64 (tiles.cu)
 };
 
 constexpr int kMaxWindows = 8;  // more windows than this -> explicit column list
@@ -39,7 +39,7 @@ struct TileMeta {      // 12 x int32
     int32_t local;     // local index space size
     int32_t own_loff;  // local index of row r0 (valid when r1 > r0)
     int32_t wt_lo, wt_hi;  // list mode: hull of owner tiles of non-own slots (wt_lo > wt_hi: none)
-    int32_t pad;
+    int32_t ev;        // max |value| of the tile's entries < 2^ev (fixed-point scale)
 };
 
 struct Window {       // 8 x int32

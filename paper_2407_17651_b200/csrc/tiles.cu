@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <new>
 
@@ -45,6 +46,9 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxTileSlices = 256;  // per-tile slice offset table in shared memory
 constexpr int kMaxSlots = 8;          // slots per slice (plan seg_max)
+constexpr int kMaxWindowsDev = pars3::kMaxWindows;
+constexpr int kLocalExact = 3200;  // window slots per tile: x + fp64 acc (16 B/slot)
+constexpr int kLocalFixed = 2496;  // x + three uint32 words (20 B/slot)
 
 struct DevPlan {
     const TileMeta *tiles;
@@ -170,22 +174,120 @@ __device__ __forceinline__ void bulk_reduce_add(double *g, const double *s, uint
                  : "memory");
 }
 
+// Issue the x-window copies of tile t (window mode) into xs; every tile
+// arrives once on xbar (list-mode and past-the-end tiles with 0 bytes) so
+// the barrier's phases count tiles.
+__device__ __forceinline__ void issue_x(const DevPlan &P, const double *x, int32_t t, double *xs,
+                                       uint64_t *xbar) {
+    uint32_t bytes = 0;
+    int w0 = 0, w1 = 0;
+    if (t < P.ntiles && __ldg(&P.tiles[t].u0) < 0) {
+        w0 = __ldg(&P.tiles[t].w0);
+        w1 = __ldg(&P.tiles[t].w1);
+        for (int w = w0; w < w1; w++) {
+            const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len);
+            if (tma_window(lo, len)) bytes += (uint32_t)len * 8;
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_tx(xbar, bytes);
+    for (int w = w0; w < w1; w++) {
+        const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
+                  off = __ldg(&P.wins[w].loff);
+        if (tma_window(lo, len)) bulk_load(xs + off, x + lo, (uint32_t)len * 8, xbar);
+    }
+}
+
+// The next tile's x-window list, cached in shared memory by thread 0 while
+// the current tile streams, so the TMA issue after the flush costs no
+// global round trip.
+struct NextWins {
+    int32_t n;  // windows (window mode), 0 for list mode / no tile
+    int32_t s0, s1;
+    int32_t lo[kMaxWindowsDev], len[kMaxWindowsDev], off[kMaxWindowsDev];
+};
+
+__device__ __forceinline__ void fetch_next(const DevPlan &P, int32_t tn, NextWins &nw) {
+    nw.n = 0;
+    nw.s0 = nw.s1 = 0;
+    if (tn >= P.ntiles) return;
+    const TileMeta m = P.tiles[tn];
+    nw.s0 = m.s0;
+    nw.s1 = m.s1;
+    if (m.u0 >= 0) return;
+    nw.n = m.w1 - m.w0;
+    for (int w = 0; w < nw.n; w++) {
+        nw.lo[w] = __ldg(&P.wins[m.w0 + w].lo);
+        nw.len[w] = __ldg(&P.wins[m.w0 + w].len);
+        nw.off[w] = __ldg(&P.wins[m.w0 + w].loff);
+    }
+}
+
+__device__ __forceinline__ void issue_x_cached(const double *x, const NextWins &nw, double *xs,
+                                              uint64_t *xbar) {
+    uint32_t bytes = 0;
+    for (int w = 0; w < nw.n; w++)
+        if (tma_window(nw.lo[w], nw.len[w])) bytes += (uint32_t)nw.len[w] * 8;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_tx(xbar, bytes);
+    for (int w = 0; w < nw.n; w++)
+        if (tma_window(nw.lo[w], nw.len[w]))
+            bulk_load(xs + nw.off[w], x + nw.lo[w], (uint32_t)nw.len[w] * 8, xbar);
+}
+
+// ---- fixed-point accumulation ---------------------------------------------
+// A slot's mirror sum is kept as an exact integer Q * 2^(E-50) in three
+// 32-bit words (bits 0-19, 20-39, 40+ signed) updated with native
+// shared-memory integer adds (fire-and-forget ATOMS.ADD, no CAS loop).
+// E = ev + ex + 3 bounds every term of the tile (|v| < 2^ev, |x| < 2^ex,
+// a row segment sums <= 8 terms), so |Q| < 2^50 per term, each word takes up
+// to 4096 terms (a tile has <= 1024 rows), and the per-term rounding is
+// <= 2^(E-51).  Integer adds commute: a tile's accumulation is independent of
+// the order in which its warps arrive.
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr long long kMagicBits = 0x4338000000000000ll;
+
+__device__ __forceinline__ void fx_add(uint32_t *lo, uint32_t *mid, uint32_t *hi, int i, double qs) {
+    // qs = value * 2^(50-E), |qs| < 2^51: the magic add leaves rint(qs) in the low mantissa bits
+    const long long Q = __double_as_longlong(qs + kMagic) - kMagicBits;
+    atomicAdd(lo + i, (uint32_t)Q & 0xFFFFFu);
+    atomicAdd(mid + i, (uint32_t)(Q >> 20) & 0xFFFFFu);
+    atomicAdd(hi + i, (uint32_t)(Q >> 40));
+}
+
+__device__ __forceinline__ double fx_value(uint32_t lo, uint32_t mid, uint32_t hi, double unscale) {
+    const long long V = ((long long)(int32_t)hi << 40) + ((long long)mid << 20) + (long long)lo;
+    return (double)V * unscale;
+}
+
+template <bool kFixed>
 __global__ void __launch_bounds__(kThreads, 4)
 k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t epoch) {
     extern __shared__ __align__(128) uint8_t dyn[];
     double *xs = reinterpret_cast<double *>(dyn);
+    // exact mode: fp64 acc[lmax]; fixed mode: three uint32 words per slot
     double *acc = xs + P.lmax;
-    __shared__ int64_t s_off[kMaxTileSlices + 1];
-    __shared__ int32_t s_tile;
+    uint32_t *wlo = reinterpret_cast<uint32_t *>(xs + P.lmax);
+    uint32_t *wmid = wlo + P.lmax;
+    uint32_t *whi = wmid + P.lmax;
+    __shared__ int64_t s_off[2][kMaxTileSlices + 1];
+    __shared__ int32_t s_t[2];
+    __shared__ int32_t s_ex[2];
     __shared__ __align__(8) uint64_t xbar;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < P.lmax; i += kThreads) acc[i] = 0.0;
+    __shared__ NextWins s_next;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (kFixed) {
+        for (int i = tid; i < P.lmax; i += kThreads) wlo[i] = wmid[i] = whi[i] = 0u;
+    } else {
+        for (int i = tid; i < P.lmax; i += kThreads) acc[i] = 0.0;
+    }
     if (tid == 0) {
         mbar_init(&xbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_t[0] = atomicAdd(P.counter, 1);
+        s_ex[0] = s_ex[1] = -1100;
     }
-    // PARS3_PHASES=1: thread 0 accumulates SM cycles per phase (claim,
-    // windows, stream, finish+store, wait, flush)
+    // PARS3_PHASES=1: thread 0 accumulates SM cycles per phase
     long long clk[6] = {0, 0, 0, 0, 0, 0};
     long long tprev = clock64();
 #define PHASE(k)                                  \
@@ -196,37 +298,29 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
             tprev = now;                          \
         }                                         \
     } while (0)
-
     __syncthreads();
-    uint32_t xphase = 0;  // completed phases of xbar (window-mode tiles only)
-    for (;;) {
-        if (tid == 0) s_tile = atomicAdd(P.counter, 1);
-        __syncthreads();
-        PHASE(0);
-        const int32_t t = s_tile;
+    {
+        const int32_t t0 = s_t[0];
+        if (t0 < P.ntiles) {
+            const int s0 = __ldg(&P.tiles[t0].s0), n0 = __ldg(&P.tiles[t0].s1) - s0;
+            for (int i = tid; i <= n0; i += kThreads) s_off[0][i] = __ldg(P.slice_off + s0 + i);
+        }
+        if (tid == 0) issue_x(P, x, t0, xs, &xbar);
+    }
+
+    for (int k = 0;; k++) {
+        const int cur = k & 1, nxt = cur ^ 1;
+        const int32_t t = s_t[cur];
         if (t >= P.ntiles) break;
         const TileMeta m = P.tiles[t];
         const int nown = m.r1 - m.r0;
         const int nsl = m.s1 - m.s0;
+        if (tid == 0) s_t[nxt] = atomicAdd(P.counter, 1);  // claim the next tile ahead
+        PHASE(0);
 
-        // 1. slice offsets; x over the tile's local slots -> shared memory:
-        //    windows by TMA bulk copies (one round trip for the whole tile),
-        //    odd-aligned windows and list-mode slots by the threads
-        if (m.u0 < 0 && tid == 0) {
-            uint32_t bytes = 0;
-            for (int w = m.w0; w < m.w1; w++) {
-                const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len);
-                if (tma_window(lo, len)) bytes += (uint32_t)len * 8;
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive_tx(&xbar, bytes);
-            for (int w = m.w0; w < m.w1; w++) {
-                const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
-                          off = __ldg(&P.wins[w].loff);
-                if (tma_window(lo, len)) bulk_load(xs + off, x + lo, (uint32_t)len * 8, &xbar);
-            }
-        }
-        for (int i = tid; i <= nsl; i += kThreads) s_off[i] = __ldg(P.slice_off + m.s0 + i);
+        // 1. x over the tile's local slots: windows arrived by TMA (issued at
+        //    the end of the previous tile), odd-aligned windows and list-mode
+        //    slots loaded here
         if (m.u0 >= 0) {
             const int32_t *uc = P.ucol + m.u0;
             for (int i = tid; i < m.local; i += kThreads) xs[i] = __ldg(x + __ldg(uc + i));
@@ -237,17 +331,38 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
                 if (!tma_window(lo, len))
                     for (int i = tid; i < len; i += kThreads) xs[off + i] = __ldg(x + lo + i);
             }
-            mbar_wait(&xbar, (uint32_t)(xphase & 1), P.watchdog, 5, t);
-            xphase++;
+        }
+        mbar_wait(&xbar, (uint32_t)(k & 1), P.watchdog, 5, t);
+        asm volatile("cp.async.wait_all;" ::: "memory");  // this tile's record offsets
+        if (kFixed) {  // tile-wide bound on |x|: max binary exponent over the slots
+            int e = -1100;
+            for (int i = tid; i < m.local; i += kThreads) {
+                const int be = (int)((__double_as_longlong(xs[i]) >> 52) & 0x7FF);
+                e = max(e, be - 1022);  // |x| < 2^(be - 1022) for normal x
+            }
+            e = __reduce_max_sync(0xffffffffu, e);
+            if (lane == 0) atomicMax(&s_ex[cur], e);
         }
         __syncthreads();
         PHASE(1);
+        if (tid == 0) {
+            fetch_next(P, s_t[nxt], s_next);  // overlaps the stream
+            s_ex[nxt] = -1100;
+        }
+        int E = 0;
+        double scale = 0.0, unscale = 0.0;
+        if (kFixed) {
+            E = m.ev + s_ex[cur] + 3;
+            E = max(-1000, min(1000, E));
+            scale = ldexp(1.0, 50 - E);
+            unscale = ldexp(1.0, E - 50);
+        }
 
         // 2. records: each lane owns one row segment of a slice; row sums in
-        //    registers, mirrors into acc (shared-memory fp64 atomics)
+        //    registers, mirrors into the tile's shared accumulators
         for (int i = warp; i < nsl; i += kWarps) {
-            const uint8_t *rp = P.rec + s_off[i] * 16;
-            const int ns = (int)(((s_off[i + 1] - s_off[i]) * 16 - 64) / 320);
+            const uint8_t *rp = P.rec + s_off[cur][i] * 16;
+            const int ns = (int)(((s_off[cur][i + 1] - s_off[cur][i]) * 16 - 64) / 320);
             const uint16_t rl = __ldcs(reinterpret_cast<const uint16_t *>(rp) + lane);
             const double *vp = reinterpret_cast<const double *>(rp + 64) + lane;
             const uint16_t *ip = reinterpret_cast<const uint16_t *>(rp + 64 + ns * 256) + lane;
@@ -264,103 +379,79 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
             }
             const double xr = rl != kNo ? xs[rl] : 0.0;
             double racc = 0.0;
+            if (kFixed) {
+                const double nxs = -xr * scale;  // mirror term v * (-x_r), scaled
 #pragma unroll
-            for (int u = 0; u < kMaxSlots; u++) entry(v[u], li[u], xr, xs, acc, racc);
-            if (rl != kNo) atomicAdd(&acc[rl], racc);
+                for (int u = 0; u < kMaxSlots; u++) {
+                    if (li[u] != kNo) {
+                        racc = fma(v[u], xs[li[u]], racc);
+                        fx_add(wlo, wmid, whi, li[u], v[u] * nxs);
+                    }
+                }
+                if (rl != kNo) fx_add(wlo, wmid, whi, rl, racc * scale);
+            } else {
+#pragma unroll
+                for (int u = 0; u < kMaxSlots; u++) entry(v[u], li[u], xr, xs, acc, racc);
+                if (rl != kNo) atomicAdd(&acc[rl], racc);
+            }
         }
         __syncthreads();
         PHASE(2);
 
-        // 3. finish the slots; own rows add diag * x
+        // 3. deliver: every slot's value (own rows + diag * x) reduces into y
+        //    with a fire-and-forget fp64 red (consecutive slots -> coalesced
+        //    L2 reductions); the accumulators are cleared in the same pass
+        const int32_t tn = s_t[nxt];
+        auto take = [&](int i) -> double {
+            if (kFixed) {
+                const double a = fx_value(wlo[i], wmid[i], whi[i], unscale);
+                wlo[i] = wmid[i] = whi[i] = 0u;
+                return a;
+            }
+            const double a = acc[i];
+            acc[i] = 0.0;
+            return a;
+        };
         if (m.u0 >= 0) {
             const int32_t *uc = P.ucol + m.u0;
             const int nmsg = m.local - nown;  // own rows are the tail of the list
-            if (P.accumulate) {
-                for (int i = tid; i < m.local; i += kThreads) {
-                    double a = acc[i];
-                    acc[i] = 0.0;
-                    if (i >= nmsg)
-                        a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + m.r0 + (i - nmsg)), xs[i], a);
-                    if (a != 0.0) atomicAdd(y + __ldg(uc + i), a);
-                }
-                __syncthreads();
-                continue;
-            }
-            for (int i = nmsg + tid; i < m.local; i += kThreads) {
-                y[m.r0 + (i - nmsg)] = fma(
-                    P.diag_const ? P.diag_alpha : __ldg(P.diag + m.r0 + (i - nmsg)), xs[i], acc[i]);
-                acc[i] = 0.0;
-            }
-        } else {
             for (int i = tid; i < m.local; i += kThreads) {
-                double a = acc[i];
-                acc[i] = 0.0;
-                const int r = m.r0 + (i - m.own_loff);
-                const bool own = i >= m.own_loff && i < m.own_loff + nown;
-                if (own) a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + r), xs[i], a);
-                if (own && !P.accumulate) y[r] = a;  // ordered: the owner stores first
-                xs[i] = (own && !P.accumulate) ? 0.0 : a;
-            }
-        }
-        if (!P.accumulate) {
-            __threadfence();
-            __syncthreads();
-            PHASE(3);
-            if (tid == 0) st_release(P.flags + t, epoch);
-            // 4. wait until the owners of every message target have stored
-            if (warp == 0) {
-                if (m.u0 >= 0) {
-                    for (int u = m.wt_lo + lane; u <= m.wt_hi; u += 32)
-                        if (u != t) wait_flag(P.flags, u, epoch, t, P.watchdog);
-                } else {
-                    for (int w = m.w0 + lane; w < m.w1; w += 32) {
-                        const int tl = __ldg(&P.wins[w].t_lo), th = __ldg(&P.wins[w].t_hi);
-                        for (int u = tl; u <= th; u++)
-                            if (u != t) wait_flag(P.flags, u, epoch, t, P.watchdog);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        PHASE(4);
-
-        // 5. deliver: list mode by reductions, window mode by one bulk
-        //    reduction per window (odd-aligned windows by hand)
-        if (m.u0 >= 0) {
-            const int32_t *uc = P.ucol + m.u0;
-            const int nmsg = m.local - nown;
-            for (int i = tid; i < nmsg; i += kThreads) {
-                const double a = acc[i];
-                acc[i] = 0.0;
+                double a = take(i);
+                if (i >= nmsg)
+                    a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + m.r0 + (i - nmsg)), xs[i], a);
                 if (a != 0.0) atomicAdd(y + __ldg(uc + i), a);
             }
         } else {
-            if (tid == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                for (int w = m.w0; w < m.w1; w++) {
-                    const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
-                              off = __ldg(&P.wins[w].loff);
-                    if (tma_window(lo, len)) bulk_reduce_add(y + lo, xs + off, (uint32_t)len * 8);
-                }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
             for (int w = m.w0; w < m.w1; w++) {
                 const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
                           off = __ldg(&P.wins[w].loff);
-                if (!tma_window(lo, len))
-                    for (int i = tid; i < len; i += kThreads)
-                        if (xs[off + i] != 0.0) atomicAdd(y + lo + i, xs[off + i]);
+                for (int i = tid; i < len; i += kThreads) {
+                    const int c = lo + i;
+                    double a = take(off + i);
+                    if (c >= m.r0 && c < m.r1)
+                        a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), xs[off + i], a);
+                    if (a != 0.0) atomicAdd(y + c, a);
+                }
             }
-            // xs is rewritten by the next tile: wait until the bulk reductions read it
-            if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
         __syncthreads();
-        PHASE(5);
+        PHASE(3);
+        // 4. the next tile: x windows into the now-free xs, record offsets
+        if (tid == 0) issue_x_cached(x, s_next, xs, &xbar);
+        if (tn < P.ntiles) {  // async copies (LDGSTS): waited for before the next stream
+            const int s0n = s_next.s0, nn = s_next.s1 - s0n;
+            for (int i = tid; i <= nn; i += kThreads)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr(&s_off[nxt][i])),
+                             "l"(P.slice_off + s0n + i)
+                             : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        PHASE(4);
     }
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (P.phase_clk && tid == 0)
         for (int k = 0; k < 6; k++) atomicAdd(P.phase_clk + k, (unsigned long long)clk[k]);
 #undef PHASE
+    (void)epoch;
 }
 
 __global__ void k_dot(int32_t n, const double *__restrict__ a, const double *__restrict__ b,
@@ -405,7 +496,7 @@ struct pars3_plan {
     int32_t *ucol = nullptr;
     int32_t stage_bytes = 0;
     double *diag = nullptr;
-    int32_t accumulate = 0, list_tiles = 0, watchdog = 0, diag_const = 0;
+    int32_t accumulate = 0, list_tiles = 0, watchdog = 0, diag_const = 0, exact = 0;
     double diag_alpha = 0.0;
     int32_t *trace_host = nullptr, *trace_dev = nullptr;
     unsigned long long *phase_clk = nullptr;
@@ -437,15 +528,27 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         if (opt->gap >= 0) o.gap = opt->gap;
         if (opt->mode > 0) o.mode = opt->mode;
     }
-    // the shared-memory budget (per-warp record rings + x/acc windows) caps both
+    // accumulation: mode 2 = exact fp64 (shared fp64 atomics), mode 1 =
+    // exact-integer fixed point, mode 0 = auto: fp64 for window-structured
+    // matrices (few conflicts, bigger tiles), fixed point when most tiles are
+    // unstructured list tiles
+    const int req_mode = opt ? opt->mode : 0;
+    bool exact = req_mode != 1;
+    // the shared-memory budget (x + accumulators per slot, 4 CTAs / SM) caps both
     if (o.seg_max > 8) o.seg_max = 8;
-    if (o.local_slots > 3200) o.local_slots = 3200;
-    o.max_segments = 32 * kMaxTileSlices;
-    if (o.seg_max > kMaxSlots) o.seg_max = kMaxSlots;
+    const int32_t want_local = o.local_slots;
+    o.local_slots = std::min(want_local, exact ? kLocalExact : kLocalFixed);
     HostPlan hp;
     int rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
                                     s->outer_row, s->outer_col, s->outer_val, o, hp);
     if (rc) return rc;
+    if (req_mode == 0 && 4ll * hp.list_tiles > (int64_t)hp.tiles.size()) {
+        exact = false;
+        o.local_slots = std::min(want_local, kLocalFixed);
+        rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
+                                    s->outer_row, s->outer_col, s->outer_val, o, hp);
+        if (rc) return rc;
+    }
     pars3_plan *pl = new (std::nothrow) pars3_plan;
     if (!pl) PARS3_FAIL(PARS3_ERR_NOMEM, "out of host memory");
     pl->n = s->n;
@@ -460,6 +563,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     pl->stage_bytes = 64 + 320 * (hp.max_nslots > 0 ? hp.max_nslots : 1);
     pl->nwins = (int64_t)hp.wins.size();
     pl->list_tiles = hp.list_tiles;
+    pl->exact = exact ? 1 : 0;
     {
         const char *wd = getenv("PARS3_WATCHDOG");
         pl->watchdog = (wd && wd[0] == '1') ? 1 : 0;
@@ -481,9 +585,9 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     // L2-sized or the matrix is unstructured; ordered mode (owner stores,
     // later tiles reduce after the owner's flag) otherwise -- DESIGN.md
     if (const char *md = getenv("PARS3_MODE")) o.mode = atoi(md);  // debug override
-    if (o.mode == 1) pl->accumulate = 0;
-    else if (o.mode == 2) pl->accumulate = 1;
-    else pl->accumulate = 1;  // measured faster at every BASELINE config
+    // the kernel accumulates every contribution into a zeroed y (the
+    // owner-stores-first "ordered" variant measured slower and was retired)
+    pl->accumulate = 1;
     std::vector<double> diag(s->diag, s->diag + s->n);
     pl->diag_const = 1;
     pl->diag_alpha = s->n ? diag[0] : 0.0;
@@ -511,16 +615,20 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         delete pl;
         PARS3_FAIL(PARS3_ERR_CUDA, "cudaMalloc failed");
     }
-    pl->smem = sizeof(double) * 2 * (size_t)pl->lmax;
+    pl->smem = (pl->exact ? 16 : 20) * (size_t)pl->lmax;
     // the attribute is per function, shared by every plan: set it to the
     // largest window space any plan may use, not to this plan's size
-    cudaError_t e = cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(double) * 2 * 3200));
+    cudaError_t e = cudaFuncSetAttribute(k_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         16 * kLocalExact);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 20 * kLocalFixed);
     int per_sm = 0, sms = 0, dev = 0;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiles, kThreads, pl->smem);
+        e = pl->exact ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiles<false>, kThreads, pl->smem)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiles<true>, kThreads, pl->smem);
     if (e != cudaSuccess || per_sm < 1) {
         delete pl;
         PARS3_FAIL(PARS3_ERR_CUDA, "tile kernel cannot be resident (smem %zu B): %s", pl->smem,
@@ -539,11 +647,14 @@ static int launch_tiles(pars3_plan *pl, const double *x, double *y, cudaStream_t
         CUDA_TRY(cudaMemsetAsync(pl->flags, 0, sizeof(int32_t) * pl->ntiles, st));
     }
     CUDA_TRY(cudaMemsetAsync(pl->counter, 0, sizeof(int32_t), st));
-    if (pl->accumulate) CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)pl->n, st));
+    CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)pl->n, st));
     DevPlan P{pl->tiles,   pl->wins,    pl->slice_off, pl->rec,  pl->ucol,        pl->diag,
               pl->flags,   pl->counter, pl->ntiles,    pl->lmax, pl->stage_bytes, pl->accumulate,
               pl->watchdog, pl->diag_const, pl->diag_alpha, pl->trace_dev, pl->phase_clk};
-    k_tiles<<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
+    if (pl->exact)
+        k_tiles<false><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
+    else
+        k_tiles<true><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
     LAUNCH_CHECK();
     return PARS3_OK;
 }
