@@ -118,6 +118,20 @@ int pars3_plan_trace(const pars3_plan *plan, int32_t **host);
  * PARS3_PHASES=1; claim, windows, stream, store, wait, flush). */
 int pars3_plan_phases(const pars3_plan *plan, int64_t *out6);
 
+/* ------------------------------------------------ MRS iteration kernels */
+
+/* Fused vector passes of one MRS iteration (paper_2407_17651_b200/mrs.py;
+ * no reference counterpart, SPEC.md:16 -- the paper's motivating solver,
+ * PAPER.md:49).  All device pointers, length n, on `stream`.
+ * pars3_mrs_lanczos: w <- y - alpha*v + gamma*w and *norm2 = <w, w>.
+ * pars3_mrs_update:  d <- (v - r0*dm2 - r1*dm1) * inv_r2 stored into dm2,
+ *                    x += tau * d, u *= inv_gamma. */
+int pars3_mrs_lanczos(int64_t n, const double *y, const double *v, double *w, double alpha,
+                      double gamma, double *norm2, void *stream);
+int pars3_mrs_update(int64_t n, double *u, double inv_gamma, const double *v, double *dm2,
+                     const double *dm1, double r0, double r1, double inv_r2, double tau,
+                     double *x, void *stream);
+
 /* --------------------------------------------- host-native preprocessing */
 
 /* Symmetrised off-diagonal adjacency of an SSS pattern: replaces

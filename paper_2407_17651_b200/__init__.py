@@ -16,6 +16,7 @@ in libpars3.so (include/pars3.h).  There is no CPU fallback for products.
 from .formats import (CooMatrix, DiagonalError, SkewReport, SkewSymmetryError, SssMatrix,
                       StructuralError, as_vector, coo_normalize, coo_to_sss, sss_to_coo,
                       validate_skew)
+from .mrs import MrsResult, mrs_solve
 from .parallel import prepare, spmv_atomic, spmv_pars3
 from .reorder import (AdjacencyPattern, Permutation, apply_permutation, compute_bandwidth,
                       pattern_from_coo, pattern_from_sss, permute_sss, rcm_order)
@@ -26,7 +27,7 @@ from .split import (BandSplit, ConflictReport, PartitionPlan, classify_conflicts
 __version__ = "0.1.0"
 
 __all__ = [
-    "AdjacencyPattern", "BandSplit", "ConflictReport", "CooMatrix", "DiagonalError", "OpCounter",
+    "AdjacencyPattern", "BandSplit", "MrsResult", "mrs_solve", "ConflictReport", "CooMatrix", "DiagonalError", "OpCounter",
     "PartitionPlan", "Permutation", "SkewReport", "SkewSymmetryError", "SssMatrix",
     "StructuralError", "apply_permutation", "as_vector", "classify_conflicts",
     "compute_bandwidth", "conflict_report", "coo_normalize", "coo_to_sss", "count_ops",

@@ -59,6 +59,11 @@ _SIGS = {
     "pars3_plan_destroy": (ctypes.c_int, [_vp]),
     "pars3_plan_trace": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     "pars3_plan_phases": (ctypes.c_int, [_vp, _vp]),
+    "pars3_mrs_lanczos": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, ctypes.c_double, ctypes.c_double,
+                                         _vp, _vp]),
+    "pars3_mrs_update": (ctypes.c_int, [_c_i64, _vp, ctypes.c_double, _vp, _vp, _vp,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_double, _vp, _vp]),
     "pars3_pattern_from_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
     "pars3_rcm_order": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, ctypes.c_int]),
     "pars3_permute_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
