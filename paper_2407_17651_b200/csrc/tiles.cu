@@ -454,17 +454,36 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
     (void)epoch;
 }
 
-__global__ void k_dot(int32_t n, const double *__restrict__ a, const double *__restrict__ b,
-                      double *out) {
+// <a, b>: 16-byte loads, four in flight per thread, one fp64 atomic per block
+__global__ void __launch_bounds__(512) k_dot(int32_t n, const double *__restrict__ a,
+                                             const double *__restrict__ b, double *out) {
     double s = 0.0;
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        s = fma(a[i], b[i], s);
+    const int64_t n2 = n / 2;
+    const double2 *a2 = reinterpret_cast<const double2 *>(a);
+    const double2 *b2 = reinterpret_cast<const double2 *>(b);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+        double2 x[4], z[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            x[u] = __ldcs(a2 + i + u * stride);
+            z[u] = __ldcs(b2 + i + u * stride);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) s = fma(x[u].y, z[u].y, fma(x[u].x, z[u].x, s));
+    }
+    for (; i < n2; i += stride) {
+        const double2 x = __ldcs(a2 + i), z = __ldcs(b2 + i);
+        s = fma(x.y, z.y, fma(x.x, z.x, s));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) s = fma(a[n - 1], b[n - 1], s);
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    __shared__ double ws[32];
+    __shared__ double ws[16];
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x < 32) {
-        s = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+        s = threadIdx.x < 16 ? ws[threadIdx.x] : 0.0;
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (threadIdx.x == 0) atomicAdd(out, s);
     }
@@ -672,7 +691,9 @@ extern "C" int pars3_plan_spmv_dot(pars3_plan *pl, const double *x, double *y, c
     if (rc) return rc;
     CUDA_TRY(cudaMemsetAsync(dot, 0, sizeof(double), st));
     if (pl->n > 0) {
-        k_dot<<<592, 512, 0, st>>>((int32_t)pl->n, y, w, dot);
+        // 16-byte loads need 16-byte aligned vectors (torch allocations are)
+        if (((uintptr_t)y | (uintptr_t)w) & 15) PARS3_FAIL(PARS3_ERR_ARG, "y and w must be 16-byte aligned");
+        k_dot<<<148 * 4, 512, 0, st>>>((int32_t)pl->n, y, w, dot);
         LAUNCH_CHECK();
     }
     return PARS3_OK;
