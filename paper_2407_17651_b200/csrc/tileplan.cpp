@@ -49,7 +49,7 @@ struct Built {               // one draft materialised
     std::vector<int32_t> ucol;
     std::vector<int64_t> slice_off;  // relative, bytes
     std::vector<uint8_t> rec;
-    int32_t r0, r1, local, own_loff, max_nslots = 0;
+    int32_t r0, r1, local, own_loff, max_nslots = 0, max_terms = 0;
     int64_t nnz, slots;
     double vmax = 0.0;
 };
@@ -184,6 +184,8 @@ void materialise(const Rows &R, const Draft &d, const PlanOptions &o, Built &b) 
                      [](const Seg &x, const Seg &y) { return (x.ke - x.kb) > (y.ke - y.kb); });
     b.nnz = 0;
     b.slots = 0;
+    // accumulator terms per local slot: one per mirror, one per row segment
+    std::vector<int32_t> terms((size_t)d.local, 0);
     for (size_t s0 = 0; s0 < segs.size(); s0 += 32) {
         size_t s1 = std::min(segs.size(), s0 + 32);
         const int32_t nslots = (int32_t)(segs[s0].ke - segs[s0].kb);
@@ -194,8 +196,10 @@ void materialise(const Rows &R, const Draft &d, const PlanOptions &o, Built &b) 
         uint16_t *rowl = reinterpret_cast<uint16_t *>(&b.rec[off]);
         double *val = reinterpret_cast<double *>(&b.rec[off + 64]);
         uint16_t *lidx = reinterpret_cast<uint16_t *>(&b.rec[off + 64 + (size_t)nslots * 256]);
-        for (size_t l = 0; l < 32; l++)
+        for (size_t l = 0; l < 32; l++) {
             rowl[l] = s0 + l < s1 ? (uint16_t)local_of(d, b.wloff, segs[s0 + l].row) : kNoSlot;
+            if (rowl[l] != kNoSlot) terms[rowl[l]]++;
+        }
         for (int64_t q = 0; q < (int64_t)nslots * 32; q++) {
             val[q] = 0.0;
             lidx[q] = kNoSlot;
@@ -207,11 +211,13 @@ void materialise(const Rows &R, const Draft &d, const PlanOptions &o, Built &b) 
                 val[pos] = R.val(sg.row, k);
                 b.vmax = std::max(b.vmax, std::fabs(val[pos]));
                 lidx[pos] = (uint16_t)local_of(d, b.wloff, R.col(sg.row, k));
+                terms[lidx[pos]]++;
                 b.nnz++;
             }
         }
         b.slots += (int64_t)nslots * 32;
     }
+    for (int32_t c : terms) b.max_terms = std::max(b.max_terms, c);
 }
 
 }  // namespace
@@ -339,7 +345,10 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
         P.slots = slots_total;
         P.slice_off[ns] = nv / 16;
         for (auto &m : P.tiles) P.max_local = std::max(P.max_local, m.local);
-        for (auto &b : built) P.max_nslots = std::max(P.max_nslots, b.max_nslots);
+        for (auto &b : built) {
+            P.max_nslots = std::max(P.max_nslots, b.max_nslots);
+            P.max_terms = std::max(P.max_terms, b.max_terms);
+        }
     } catch (const std::bad_alloc &) {
         PARS3_FAIL(PARS3_ERR_NOMEM, "tile plan: out of host memory");
     }

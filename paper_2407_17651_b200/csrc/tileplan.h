@@ -26,7 +26,8 @@ struct PlanOptions {
     int32_t seg_max = 8;        // max entries per row segment (longer rows are split)
     int32_t gap = 8;            // merge column runs separated by <= gap unused slots
     int32_t max_segments = 16384;  // row segments per tile (the kernel's slice table bound / 32)
-    int32_t mode = 0;           // accumulation: 0 auto, 1 fixed point, 2 fp64 (tiles.cu)
+    int32_t mode = 0;           // accumulation: 0 auto, 1 fixed point (3 words), 2 fp64,
+                                // 3 fixed point (2 words) (tiles.cu)
 };
 
 constexpr int kMaxWindows = 8;  // more windows than this -> explicit column list
@@ -60,6 +61,7 @@ struct HostPlan {
     int32_t max_nslots = 0;
     int32_t list_tiles = 0;
     int32_t max_local = 0;
+    int32_t max_terms = 0;              // most accumulator terms one slot takes in one tile
 };
 
 // Build from host split arrays (BandSplit layout, split.py:58-113).

@@ -47,8 +47,9 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMaxTileSlices = 256;  // per-tile slice offset table in shared memory
 constexpr int kMaxSlots = 8;          // slots per slice (plan seg_max)
 constexpr int kMaxWindowsDev = pars3::kMaxWindows;
-constexpr int kLocalExact = 3200;  // window slots per tile: x + fp64 acc (16 B/slot)
+constexpr int kLocalExact = 3200;  // window slots per tile: x + fp64 acc or two words (16 B/slot)
 constexpr int kLocalFixed = 2496;  // x + three uint32 words (20 B/slot)
+constexpr int kTerms2 = 64;        // two-word fixed point: max terms per slot per tile
 
 struct DevPlan {
     const TileMeta *tiles;
@@ -68,6 +69,10 @@ struct DevPlan {
     double diag_alpha;
     volatile int32_t *trace;  // mapped host memory, 32 ints per CTA (debug), or null
     unsigned long long *phase_clk;  // PARS3_PHASES=1: per-phase SM cycles (thread 0 of each CTA)
+    int32_t pf;  // L2 prefetch of records: bit 0 the next tile's records (claim time), bit 1 each
+                 // warp's slice pf_dist iterations ahead, bit 2 the next tile's first slices
+                 // when a warp leaves the stream
+    int32_t pf_dist;
 };
 
 // debug trace (PARS3_TRACE=1): progress markers readable by the host while the
@@ -166,6 +171,12 @@ __device__ __forceinline__ void entry(double v, uint16_t li, double xr, const do
     }
 }
 
+// TMA bulk prefetch of [p, p + bytes) into L2 (no shared memory, no registers):
+// keeps DRAM busy across a CTA's per-tile window/flush phases
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ bool tma_window(int lo, int len) { return ((lo | len) & 1) == 0; }
 
 __device__ __forceinline__ void bulk_reduce_add(double *g, const double *s, uint32_t bytes) {
@@ -214,6 +225,11 @@ __device__ __forceinline__ void fetch_next(const DevPlan &P, int32_t tn, NextWin
     const TileMeta m = P.tiles[tn];
     nw.s0 = m.s0;
     nw.s1 = m.s1;
+    if (P.pf & 1) {
+        const int64_t o0 = __ldg(P.slice_off + m.s0), o1 = __ldg(P.slice_off + m.s1);
+        for (int64_t o = o0; o < o1; o += 4096)  // 64 KB per bulk prefetch
+            bulk_prefetch_l2(P.rec + o * 16, (uint32_t)((o1 - o < 4096 ? o1 - o : 4096) * 16));
+    }
     if (m.u0 >= 0) return;
     nw.n = m.w1 - m.w0;
     for (int w = 0; w < nw.n; w++) {
@@ -260,15 +276,32 @@ __device__ __forceinline__ double fx_value(uint32_t lo, uint32_t mid, uint32_t h
     return (double)V * unscale;
 }
 
-template <bool kFixed>
+// Two-word variant for tiles whose slots each take <= kTerms2 = 64 terms
+// (the plan checks): bits 0-25 in an unsigned word (64 x 2^26 = 2^32) and
+// the signed rest (|Q| < 2^50 -> |Q >> 26| < 2^24, 64 terms < 2^30).
+__device__ __forceinline__ void fx_add2(uint32_t *lo, uint32_t *hi, int i, double qs) {
+    const long long Q = __double_as_longlong(qs + kMagic) - kMagicBits;
+    atomicAdd(lo + i, (uint32_t)Q & 0x3FFFFFFu);
+    atomicAdd(hi + i, (uint32_t)(Q >> 26));
+}
+
+__device__ __forceinline__ double fx_value2(uint32_t lo, uint32_t hi, double unscale) {
+    const long long V = ((long long)(int32_t)hi << 26) + (long long)lo;
+    return (double)V * unscale;
+}
+
+// kWords: 0 = fp64 shared accumulators (CAS loop per mirror), 2 / 3 =
+// exact-integer fixed point in two / three 32-bit words per slot
+template <int kWords>
 __global__ void __launch_bounds__(kThreads, 4)
 k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t epoch) {
+    constexpr bool kFixed = kWords > 0;
     extern __shared__ __align__(128) uint8_t dyn[];
     double *xs = reinterpret_cast<double *>(dyn);
     // exact mode: fp64 acc[lmax]; fixed mode: three uint32 words per slot
     double *acc = xs + P.lmax;
     uint32_t *wlo = reinterpret_cast<uint32_t *>(xs + P.lmax);
-    uint32_t *wmid = wlo + P.lmax;
+    uint32_t *wmid = wlo + P.lmax;  // two-word mode: the high word
     uint32_t *whi = wmid + P.lmax;
     __shared__ int64_t s_off[2][kMaxTileSlices + 1];
     __shared__ int32_t s_t[2];
@@ -276,8 +309,10 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
     __shared__ __align__(8) uint64_t xbar;
     __shared__ NextWins s_next;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (kFixed) {
+    if (kWords == 3) {
         for (int i = tid; i < P.lmax; i += kThreads) wlo[i] = wmid[i] = whi[i] = 0u;
+    } else if (kWords == 2) {
+        for (int i = tid; i < P.lmax; i += kThreads) wlo[i] = wmid[i] = 0u;
     } else {
         for (int i = tid; i < P.lmax; i += kThreads) acc[i] = 0.0;
     }
@@ -286,6 +321,7 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         s_t[0] = atomicAdd(P.counter, 1);
         s_ex[0] = s_ex[1] = -1100;
+        s_next.n = s_next.s0 = s_next.s1 = 0;  // read (racily, prefetch hints only) before the first fetch_next
     }
     // PARS3_PHASES=1: thread 0 accumulates SM cycles per phase
     long long clk[6] = {0, 0, 0, 0, 0, 0};
@@ -361,6 +397,11 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
         // 2. records: each lane owns one row segment of a slice; row sums in
         //    registers, mirrors into the tile's shared accumulators
         for (int i = warp; i < nsl; i += kWarps) {
+            if ((P.pf & 2) && lane == 0 && i + P.pf_dist * kWarps < nsl) {
+                const int j = i + P.pf_dist * kWarps;
+                const int64_t a = s_off[cur][j], b = s_off[cur][j + 1];
+                bulk_prefetch_l2(P.rec + a * 16, (uint32_t)((b - a) * 16));
+            }
             const uint8_t *rp = P.rec + s_off[cur][i] * 16;
             const int ns = (int)(((s_off[cur][i + 1] - s_off[cur][i]) * 16 - 64) / 320);
             const uint16_t rl = __ldcs(reinterpret_cast<const uint16_t *>(rp) + lane);
@@ -385,14 +426,29 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
                 for (int u = 0; u < kMaxSlots; u++) {
                     if (li[u] != kNo) {
                         racc = fma(v[u], xs[li[u]], racc);
-                        fx_add(wlo, wmid, whi, li[u], v[u] * nxs);
+                        if (kWords == 3)
+                            fx_add(wlo, wmid, whi, li[u], v[u] * nxs);
+                        else
+                            fx_add2(wlo, wmid, li[u], v[u] * nxs);
                     }
                 }
-                if (rl != kNo) fx_add(wlo, wmid, whi, rl, racc * scale);
+                if (rl != kNo) {
+                    if (kWords == 3)
+                        fx_add(wlo, wmid, whi, rl, racc * scale);
+                    else
+                        fx_add2(wlo, wmid, rl, racc * scale);
+                }
             } else {
 #pragma unroll
                 for (int u = 0; u < kMaxSlots; u++) entry(v[u], li[u], xr, xs, acc, racc);
                 if (rl != kNo) atomicAdd(&acc[rl], racc);
+            }
+        }
+        if ((P.pf & 4) && lane == 0) {  // warm L2 with the next tile's first slices
+            const int sn = s_next.s0 + warp * P.pf_dist;
+            for (int q = 0; q < P.pf_dist && sn + q < s_next.s1; q++) {
+                const int64_t a = __ldg(P.slice_off + sn + q), b = __ldg(P.slice_off + sn + q + 1);
+                bulk_prefetch_l2(P.rec + a * 16, (uint32_t)((b - a) * 16));
             }
         }
         __syncthreads();
@@ -403,9 +459,14 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
         //    L2 reductions); the accumulators are cleared in the same pass
         const int32_t tn = s_t[nxt];
         auto take = [&](int i) -> double {
-            if (kFixed) {
+            if (kWords == 3) {
                 const double a = fx_value(wlo[i], wmid[i], whi[i], unscale);
                 wlo[i] = wmid[i] = whi[i] = 0u;
+                return a;
+            }
+            if (kWords == 2) {
+                const double a = fx_value2(wlo[i], wmid[i], unscale);
+                wlo[i] = wmid[i] = 0u;
                 return a;
             }
             const double a = acc[i];
@@ -515,7 +576,7 @@ struct pars3_plan {
     int32_t *ucol = nullptr;
     int32_t stage_bytes = 0;
     double *diag = nullptr;
-    int32_t accumulate = 0, list_tiles = 0, watchdog = 0, diag_const = 0, exact = 0;
+    int32_t accumulate = 0, list_tiles = 0, watchdog = 0, diag_const = 0, words = 0, pf = 0, pf_dist = 1;
     double diag_alpha = 0.0;
     int32_t *trace_host = nullptr, *trace_dev = nullptr;
     unsigned long long *phase_clk = nullptr;
@@ -547,26 +608,33 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         if (opt->gap >= 0) o.gap = opt->gap;
         if (opt->mode > 0) o.mode = opt->mode;
     }
-    // accumulation: mode 2 = exact fp64 (shared fp64 atomics), mode 1 =
-    // exact-integer fixed point, mode 0 = auto: fp64 for window-structured
-    // matrices (few conflicts, bigger tiles), fixed point when most tiles are
-    // unstructured list tiles
+    // accumulation of the mirror sums: mode 2 = fp64 shared accumulators,
+    // mode 1 = exact-integer fixed point in three words, mode 3 = two words
+    // (needs <= kTerms2 terms per slot and tile), mode 0 = auto: two words
+    // when the plan allows, else fp64 for window-structured matrices and
+    // three words when most tiles are unstructured list tiles
     const int req_mode = opt ? opt->mode : 0;
-    bool exact = req_mode != 1;
+    int words = req_mode == 1 ? 3 : req_mode == 2 ? 0 : 2;
     // the shared-memory budget (x + accumulators per slot, 4 CTAs / SM) caps both
     if (o.seg_max > 8) o.seg_max = 8;
     const int32_t want_local = o.local_slots;
-    o.local_slots = std::min(want_local, exact ? kLocalExact : kLocalFixed);
+    o.local_slots = std::min(want_local, words == 3 ? kLocalFixed : kLocalExact);
     HostPlan hp;
     int rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
                                     s->outer_row, s->outer_col, s->outer_val, o, hp);
     if (rc) return rc;
-    if (req_mode == 0 && 4ll * hp.list_tiles > (int64_t)hp.tiles.size()) {
-        exact = false;
-        o.local_slots = std::min(want_local, kLocalFixed);
-        rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
-                                    s->outer_row, s->outer_col, s->outer_val, o, hp);
-        if (rc) return rc;
+    if (words == 2 && hp.max_terms > kTerms2) {
+        if (req_mode == 3)
+            PARS3_FAIL(PARS3_ERR_ARG, "two-word accumulation needs <= %d terms per slot, plan has %d",
+                       kTerms2, hp.max_terms);
+        words = 0;
+        if (4ll * hp.list_tiles > (int64_t)hp.tiles.size()) {
+            words = 3;
+            o.local_slots = std::min(want_local, kLocalFixed);
+            rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
+                                        s->outer_row, s->outer_col, s->outer_val, o, hp);
+            if (rc) return rc;
+        }
     }
     pars3_plan *pl = new (std::nothrow) pars3_plan;
     if (!pl) PARS3_FAIL(PARS3_ERR_NOMEM, "out of host memory");
@@ -582,10 +650,14 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     pl->stage_bytes = 64 + 320 * (hp.max_nslots > 0 ? hp.max_nslots : 1);
     pl->nwins = (int64_t)hp.wins.size();
     pl->list_tiles = hp.list_tiles;
-    pl->exact = exact ? 1 : 0;
+    pl->words = words;
     {
         const char *wd = getenv("PARS3_WATCHDOG");
         pl->watchdog = (wd && wd[0] == '1') ? 1 : 0;
+        const char *pf = getenv("PARS3_PF");
+        pl->pf = pf ? atoi(pf) : 6;  // measured best on c5 (profiles/r01/sweep_pf*.txt)
+        const char *pd = getenv("PARS3_PF_DIST");
+        pl->pf_dist = pd ? std::max(1, atoi(pd)) : 1;
         const char *ph = getenv("PARS3_PHASES");
         if (ph && ph[0] == '1') {
             cudaMalloc((void **)&pl->phase_clk, 8 * sizeof(unsigned long long));
@@ -634,20 +706,24 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         delete pl;
         PARS3_FAIL(PARS3_ERR_CUDA, "cudaMalloc failed");
     }
-    pl->smem = (pl->exact ? 16 : 20) * (size_t)pl->lmax;
+    pl->smem = (pl->words == 3 ? 20 : 16) * (size_t)pl->lmax;
     // the attribute is per function, shared by every plan: set it to the
     // largest window space any plan may use, not to this plan's size
-    cudaError_t e = cudaFuncSetAttribute(k_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_tiles<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          16 * kLocalExact);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(k_tiles<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 16 * kLocalExact);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_tiles<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  20 * kLocalFixed);
     int per_sm = 0, sms = 0, dev = 0;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
-        e = pl->exact ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiles<false>, kThreads, pl->smem)
-                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tiles<true>, kThreads, pl->smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, pl->words == 0 ? k_tiles<0> : pl->words == 2 ? k_tiles<2> : k_tiles<3>, kThreads,
+            pl->smem);
     if (e != cudaSuccess || per_sm < 1) {
         delete pl;
         PARS3_FAIL(PARS3_ERR_CUDA, "tile kernel cannot be resident (smem %zu B): %s", pl->smem,
@@ -669,11 +745,13 @@ static int launch_tiles(pars3_plan *pl, const double *x, double *y, cudaStream_t
     CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)pl->n, st));
     DevPlan P{pl->tiles,   pl->wins,    pl->slice_off, pl->rec,  pl->ucol,        pl->diag,
               pl->flags,   pl->counter, pl->ntiles,    pl->lmax, pl->stage_bytes, pl->accumulate,
-              pl->watchdog, pl->diag_const, pl->diag_alpha, pl->trace_dev, pl->phase_clk};
-    if (pl->exact)
-        k_tiles<false><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
+              pl->watchdog, pl->diag_const, pl->diag_alpha, pl->trace_dev, pl->phase_clk, pl->pf, pl->pf_dist};
+    if (pl->words == 0)
+        k_tiles<0><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
+    else if (pl->words == 2)
+        k_tiles<2><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
     else
-        k_tiles<true><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
+        k_tiles<3><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
     LAUNCH_CHECK();
     return PARS3_OK;
 }
@@ -722,7 +800,7 @@ extern "C" int pars3_plan_stats(const pars3_plan *pl, int64_t *stats) {
     stats[6] = pl->grid;
     stats[7] = pl->bytes;
     stats[8] = pl->list_tiles;
-    stats[9] = pl->accumulate;
+    stats[9] = pl->words;
     return PARS3_OK;
 }
 

@@ -104,7 +104,7 @@ class Pars3Operator:
         a = np.zeros(10, dtype=np.int64)
         _lib.check(self._L.pars3_plan_stats(self._handle, _lib.ptr(a)))
         keys = ("tiles", "slices", "padded_slots", "entries", "windows", "max_local", "grid",
-                "device_bytes", "list_tiles", "accumulate")
+                "device_bytes", "list_tiles", "accum_words")
         return {k: int(v) for k, v in zip(keys, a)}
 
     def close(self):
