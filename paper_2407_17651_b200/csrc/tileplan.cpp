@@ -197,12 +197,12 @@ void materialise(const Rows &R, const Draft &d, const PlanOptions &o, Built &b) 
         double *val = reinterpret_cast<double *>(&b.rec[off + 64]);
         uint16_t *lidx = reinterpret_cast<uint16_t *>(&b.rec[off + 64 + (size_t)nslots * 256]);
         for (size_t l = 0; l < 32; l++) {
-            rowl[l] = s0 + l < s1 ? (uint16_t)local_of(d, b.wloff, segs[s0 + l].row) : kNoSlot;
-            if (rowl[l] != kNoSlot) terms[rowl[l]]++;
+            rowl[l] = s0 + l < s1 ? (uint16_t)local_of(d, b.wloff, segs[s0 + l].row) : o.sink;
+            if (s0 + l < s1) terms[rowl[l]]++;
         }
         for (int64_t q = 0; q < (int64_t)nslots * 32; q++) {
             val[q] = 0.0;
-            lidx[q] = kNoSlot;
+            lidx[q] = o.sink;
         }
         for (size_t l = 0; l < s1 - s0; l++) {
             const Seg &sg = segs[s0 + l];
@@ -226,7 +226,8 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
                     const double *mid_val, int64_t outer_count, const int32_t *outer_row,
                     const int32_t *outer_col, const double *outer_val, const PlanOptions &o,
                     HostPlan &P) {
-    if (o.local_slots < 64 || o.local_slots > 65535 || o.tile_rows < 1 || o.seg_max < 1)
+    if (o.local_slots < 64 || o.local_slots > 65535 || o.tile_rows < 1 || o.seg_max < 1 ||
+        (o.sink != kNoSlot && o.sink < o.local_slots))
         PARS3_FAIL(PARS3_ERR_ARG, "bad plan options");
     try {
         std::vector<int64_t> optr(n + 1, 0);

@@ -28,6 +28,7 @@ struct PlanOptions {
     int32_t max_segments = 16384;  // row segments per tile (the kernel's slice table bound / 32)
     int32_t mode = 0;           // accumulation: 0 auto, 1 fixed point (3 words), 2 fp64,
                                 // 3 fixed point (2 words) (tiles.cu)
+    uint16_t sink = kNoSlot;    // local slot that padding lanes / entries point at (> local_slots)
 };
 
 constexpr int kMaxWindows = 8;  // more windows than this -> explicit column list

@@ -50,6 +50,18 @@ constexpr int kMaxWindowsDev = pars3::kMaxWindows;
 constexpr int kLocalExact = 3200;  // window slots per tile: x + fp64 acc or two words (16 B/slot)
 constexpr int kLocalFixed = 2496;  // x + three uint32 words (20 B/slot)
 constexpr int kTerms2 = 64;        // two-word fixed point: max terms per slot per tile
+// Shared arrays are laid out with a compile-time stride (so the second and
+// third accumulator words are an immediate offset from the first): the
+// plan's local space, then one spare slot and the SINK slot that padding
+// lanes and padding entries of a slice point at (x = 0, never flushed), so
+// the stream loop needs no sentinel branches.
+template <int kWords>
+struct Layout {
+    static constexpr int kCap = kWords == 3 ? kLocalFixed : kLocalExact;
+    static constexpr int kStride = kCap + 2;
+    static constexpr int kSink = kCap + 1;
+    static constexpr int kSmem = kStride * (kWords == 3 ? 20 : 16);
+};
 
 struct DevPlan {
     const TileMeta *tiles;
@@ -163,14 +175,6 @@ __device__ __forceinline__ void wait_flag(const int32_t *flags, int u, int32_t e
     }
 }
 
-__device__ __forceinline__ void entry(double v, uint16_t li, double xr, const double *xs,
-                                      double *acc, double &racc) {
-    if (li != kNo) {
-        racc = fma(v, xs[li], racc);
-        atomicAdd(&acc[li], -v * xr);
-    }
-}
-
 // TMA bulk prefetch of [p, p + bytes) into L2 (no shared memory, no registers):
 // keeps DRAM busy across a CTA's per-tile window/flush phases
 __device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
@@ -263,14 +267,6 @@ __device__ __forceinline__ void issue_x_cached(const double *x, const NextWins &
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 constexpr long long kMagicBits = 0x4338000000000000ll;
 
-__device__ __forceinline__ void fx_add(uint32_t *lo, uint32_t *mid, uint32_t *hi, int i, double qs) {
-    // qs = value * 2^(50-E), |qs| < 2^51: the magic add leaves rint(qs) in the low mantissa bits
-    const long long Q = __double_as_longlong(qs + kMagic) - kMagicBits;
-    atomicAdd(lo + i, (uint32_t)Q & 0xFFFFFu);
-    atomicAdd(mid + i, (uint32_t)(Q >> 20) & 0xFFFFFu);
-    atomicAdd(hi + i, (uint32_t)(Q >> 40));
-}
-
 __device__ __forceinline__ double fx_value(uint32_t lo, uint32_t mid, uint32_t hi, double unscale) {
     const long long V = ((long long)(int32_t)hi << 40) + ((long long)mid << 20) + (long long)lo;
     return (double)V * unscale;
@@ -279,10 +275,24 @@ __device__ __forceinline__ double fx_value(uint32_t lo, uint32_t mid, uint32_t h
 // Two-word variant for tiles whose slots each take <= kTerms2 = 64 terms
 // (the plan checks): bits 0-25 in an unsigned word (64 x 2^26 = 2^32) and
 // the signed rest (|Q| < 2^50 -> |Q >> 26| < 2^24, 64 terms < 2^30).
-__device__ __forceinline__ void fx_add2(uint32_t *lo, uint32_t *hi, int i, double qs) {
-    const long long Q = __double_as_longlong(qs + kMagic) - kMagicBits;
-    atomicAdd(lo + i, (uint32_t)Q & 0x3FFFFFFu);
-    atomicAdd(hi + i, (uint32_t)(Q >> 26));
+// q = fma(t, 2^(50-E), 1.5 * 2^52): the low mantissa bits hold rint(t * 2^(50-E))
+// = Q as a two's-complement offset from the magic constant, so the words
+// come straight from the two halves of q (bits 0-25, and Q >> 26).
+template <int kS>
+__device__ __forceinline__ void fx_add2m(uint32_t *w, uint32_t i, double q) {
+    const uint32_t blo = (uint32_t)__double2loint(q);
+    const uint32_t bhi = (uint32_t)__double2hiint(q) - 0x43380000u;  // Q >> 32
+    atomicAdd(w + i, blo & 0x3FFFFFFu);
+    atomicAdd(w + kS + i, __funnelshift_r(blo, bhi, 26));
+}
+
+template <int kS>
+__device__ __forceinline__ void fx_add3m(uint32_t *w, uint32_t i, double q) {
+    const uint32_t blo = (uint32_t)__double2loint(q);
+    const uint32_t bhi = (uint32_t)__double2hiint(q) - 0x43380000u;
+    atomicAdd(w + i, blo & 0xFFFFFu);
+    atomicAdd(w + kS + i, __funnelshift_r(blo, bhi, 20) & 0xFFFFFu);
+    atomicAdd(w + 2 * kS + i, (uint32_t)((int32_t)bhi >> 8));
 }
 
 __device__ __forceinline__ double fx_value2(uint32_t lo, uint32_t hi, double unscale) {
@@ -296,25 +306,30 @@ template <int kWords>
 __global__ void __launch_bounds__(kThreads, 4)
 k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t epoch) {
     constexpr bool kFixed = kWords > 0;
+    constexpr int S = Layout<kWords>::kStride;
+    constexpr uint32_t kSink = Layout<kWords>::kSink;
     extern __shared__ __align__(128) uint8_t dyn[];
     double *xs = reinterpret_cast<double *>(dyn);
-    // exact mode: fp64 acc[lmax]; fixed mode: three uint32 words per slot
-    double *acc = xs + P.lmax;
-    uint32_t *wlo = reinterpret_cast<uint32_t *>(xs + P.lmax);
-    uint32_t *wmid = wlo + P.lmax;  // two-word mode: the high word
-    uint32_t *whi = wmid + P.lmax;
+    // fp64 mode: acc[S]; fixed mode: two or three uint32 words per slot
+    double *acc = xs + S;
+    uint32_t *wlo = reinterpret_cast<uint32_t *>(xs + S);
+    uint32_t *wmid = wlo + S;  // two-word mode: the high word
+    uint32_t *whi = wmid + S;
     __shared__ int64_t s_off[2][kMaxTileSlices + 1];
     __shared__ int32_t s_t[2];
     __shared__ int32_t s_ex[2];
     __shared__ __align__(8) uint64_t xbar;
     __shared__ NextWins s_next;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (kWords == 3) {
-        for (int i = tid; i < P.lmax; i += kThreads) wlo[i] = wmid[i] = whi[i] = 0u;
-    } else if (kWords == 2) {
-        for (int i = tid; i < P.lmax; i += kThreads) wlo[i] = wmid[i] = 0u;
-    } else {
-        for (int i = tid; i < P.lmax; i += kThreads) acc[i] = 0.0;
+    for (int i = tid; i < S; i += kThreads) {
+        xs[i] = 0.0;  // the sink's x stays 0
+        if (kWords == 3) {
+            wlo[i] = wmid[i] = whi[i] = 0u;
+        } else if (kWords == 2) {
+            wlo[i] = wmid[i] = 0u;
+        } else {
+            acc[i] = 0.0;
+        }
     }
     if (tid == 0) {
         mbar_init(&xbar, 1);
@@ -324,13 +339,15 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
         s_next.n = s_next.s0 = s_next.s1 = 0;  // read (racily, prefetch hints only) before the first fetch_next
     }
     // PARS3_PHASES=1: thread 0 accumulates SM cycles per phase
-    long long clk[6] = {0, 0, 0, 0, 0, 0};
+    // (totals in shared memory: no registers held across the tile loop)
+    __shared__ long long s_clk[6];
+    if (tid < 6) s_clk[tid] = 0;
     long long tprev = clock64();
 #define PHASE(k)                                  \
     do {                                          \
         if (P.phase_clk && tid == 0) {            \
             const long long now = clock64();      \
-            clk[k] += now - tprev;                \
+            s_clk[k] += now - tprev;              \
             tprev = now;                          \
         }                                         \
     } while (0)
@@ -404,44 +421,55 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
             }
             const uint8_t *rp = P.rec + s_off[cur][i] * 16;
             const int ns = (int)(((s_off[cur][i + 1] - s_off[cur][i]) * 16 - 64) / 320);
-            const uint16_t rl = __ldcs(reinterpret_cast<const uint16_t *>(rp) + lane);
+            const uint32_t rl = __ldcs(reinterpret_cast<const uint16_t *>(rp) + lane);
             const double *vp = reinterpret_cast<const double *>(rp + 64) + lane;
             const uint16_t *ip = reinterpret_cast<const uint16_t *>(rp + 64 + ns * 256) + lane;
             double v[kMaxSlots];
-            uint16_t li[kMaxSlots];
+            uint32_t li[kMaxSlots];
 #pragma unroll
             for (int u = 0; u < kMaxSlots; u++) {
                 v[u] = 0.0;
-                li[u] = kNo;
-                if (u < ns) {
+                li[u] = kSink;
+                if (u < ns) {  // warp-uniform; padding entries are (0, sink)
                     v[u] = __ldcs(vp + 32 * u);
                     li[u] = __ldcs(ip + 32 * u);
                 }
             }
-            const double xr = rl != kNo ? xs[rl] : 0.0;
-            double racc = 0.0;
+            const double xr = xs[rl];
+            double r0 = 0.0, r1 = 0.0;  // two chains: even and odd slots
             if (kFixed) {
                 const double nxs = -xr * scale;  // mirror term v * (-x_r), scaled
 #pragma unroll
                 for (int u = 0; u < kMaxSlots; u++) {
-                    if (li[u] != kNo) {
-                        racc = fma(v[u], xs[li[u]], racc);
-                        if (kWords == 3)
-                            fx_add(wlo, wmid, whi, li[u], v[u] * nxs);
+                    if (u < ns) {
+                        if (u & 1)
+                            r1 = fma(v[u], xs[li[u]], r1);
                         else
-                            fx_add2(wlo, wmid, li[u], v[u] * nxs);
+                            r0 = fma(v[u], xs[li[u]], r0);
+                        const double q = fma(v[u], nxs, kMagic);
+                        if (kWords == 3)
+                            fx_add3m<S>(wlo, li[u], q);
+                        else
+                            fx_add2m<S>(wlo, li[u], q);
                     }
                 }
-                if (rl != kNo) {
-                    if (kWords == 3)
-                        fx_add(wlo, wmid, whi, rl, racc * scale);
-                    else
-                        fx_add2(wlo, wmid, rl, racc * scale);
-                }
+                const double q = fma(r0 + r1, scale, kMagic);
+                if (kWords == 3)
+                    fx_add3m<S>(wlo, rl, q);
+                else
+                    fx_add2m<S>(wlo, rl, q);
             } else {
 #pragma unroll
-                for (int u = 0; u < kMaxSlots; u++) entry(v[u], li[u], xr, xs, acc, racc);
-                if (rl != kNo) atomicAdd(&acc[rl], racc);
+                for (int u = 0; u < kMaxSlots; u++) {
+                    if (u < ns) {
+                        if (u & 1)
+                            r1 = fma(v[u], xs[li[u]], r1);
+                        else
+                            r0 = fma(v[u], xs[li[u]], r0);
+                        atomicAdd(&acc[li[u]], -v[u] * xr);
+                    }
+                }
+                atomicAdd(&acc[rl], r0 + r1);
             }
         }
         if ((P.pf & 4) && lane == 0) {  // warm L2 with the next tile's first slices
@@ -510,7 +538,7 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
         PHASE(4);
     }
     if (P.phase_clk && tid == 0)
-        for (int k = 0; k < 6; k++) atomicAdd(P.phase_clk + k, (unsigned long long)clk[k]);
+        for (int k = 0; k < 6; k++) atomicAdd(P.phase_clk + k, (unsigned long long)s_clk[k]);
 #undef PHASE
     (void)epoch;
 }
@@ -619,6 +647,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     if (o.seg_max > 8) o.seg_max = 8;
     const int32_t want_local = o.local_slots;
     o.local_slots = std::min(want_local, words == 3 ? kLocalFixed : kLocalExact);
+    o.sink = (uint16_t)(words == 3 ? Layout<3>::kSink : Layout<0>::kSink);
     HostPlan hp;
     int rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
                                     s->outer_row, s->outer_col, s->outer_val, o, hp);
@@ -631,6 +660,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         if (4ll * hp.list_tiles > (int64_t)hp.tiles.size()) {
             words = 3;
             o.local_slots = std::min(want_local, kLocalFixed);
+            o.sink = (uint16_t)Layout<3>::kSink;
             rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
                                         s->outer_row, s->outer_col, s->outer_val, o, hp);
             if (rc) return rc;
@@ -706,17 +736,17 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         delete pl;
         PARS3_FAIL(PARS3_ERR_CUDA, "cudaMalloc failed");
     }
-    pl->smem = (pl->words == 3 ? 20 : 16) * (size_t)pl->lmax;
+    pl->smem = pl->words == 0 ? Layout<0>::kSmem : pl->words == 2 ? Layout<2>::kSmem : Layout<3>::kSmem;
     // the attribute is per function, shared by every plan: set it to the
     // largest window space any plan may use, not to this plan's size
     cudaError_t e = cudaFuncSetAttribute(k_tiles<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         16 * kLocalExact);
+                                         Layout<0>::kSmem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_tiles<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 16 * kLocalExact);
+                                 Layout<2>::kSmem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_tiles<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 20 * kLocalFixed);
+                                 Layout<3>::kSmem);
     int per_sm = 0, sms = 0, dev = 0;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
