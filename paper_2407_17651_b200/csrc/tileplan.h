@@ -25,7 +25,7 @@ struct PlanOptions {
     int32_t local_slots = 3200; // shared-memory window slots per tile (x + acc = 16 B each)
     int32_t seg_max = 8;        // max entries per row segment (longer rows are split)
     int32_t gap = 8;            // merge column runs separated by <= gap unused slots
-    int32_t max_segments = 16384;  // row segments per tile (the kernel's slice table bound / 32)
+    int32_t max_segments = 8192;   // row segments per tile (32 x the kernel's 256-slice table)
     int32_t mode = 0;           // accumulation: 0 auto, 1 fixed point (3 words), 2 fp64,
                                 // 3 fixed point (2 words) (tiles.cu)
     uint16_t sink = kNoSlot;    // local slot that padding lanes / entries point at (> local_slots)

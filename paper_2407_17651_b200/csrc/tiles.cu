@@ -189,70 +189,61 @@ __device__ __forceinline__ void bulk_reduce_add(double *g, const double *s, uint
                  : "memory");
 }
 
-// Issue the x-window copies of tile t (window mode) into xs; every tile
-// arrives once on xbar (list-mode and past-the-end tiles with 0 bytes) so
-// the barrier's phases count tiles.
-__device__ __forceinline__ void issue_x(const DevPlan &P, const double *x, int32_t t, double *xs,
-                                       uint64_t *xbar) {
-    uint32_t bytes = 0;
-    int w0 = 0, w1 = 0;
-    if (t < P.ntiles && __ldg(&P.tiles[t].u0) < 0) {
-        w0 = __ldg(&P.tiles[t].w0);
-        w1 = __ldg(&P.tiles[t].w1);
-        for (int w = w0; w < w1; w++) {
-            const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len);
-            if (tma_window(lo, len)) bytes += (uint32_t)len * 8;
-        }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive_tx(xbar, bytes);
-    for (int w = w0; w < w1; w++) {
-        const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
-                  off = __ldg(&P.wins[w].loff);
-        if (tma_window(lo, len)) bulk_load(xs + off, x + lo, (uint32_t)len * 8, xbar);
-    }
-}
-
-// The next tile's x-window list, cached in shared memory by thread 0 while
-// the current tile streams, so the TMA issue after the flush costs no
-// global round trip.
-struct NextWins {
-    int32_t n;  // windows (window mode), 0 for list mode / no tile
-    int32_t s0, s1;
+// One tile's metadata and x-window list, copied into shared memory by
+// thread 0 one tile ahead (while the previous tile streams), so neither the
+// TMA issue nor the flush pays a global round trip.
+struct TileCache {
+    TileMeta m;
+    int32_t nw;  // windows (window mode), 0 for list mode / past the end
     int32_t lo[kMaxWindowsDev], len[kMaxWindowsDev], off[kMaxWindowsDev];
 };
 
-__device__ __forceinline__ void fetch_next(const DevPlan &P, int32_t tn, NextWins &nw) {
-    nw.n = 0;
-    nw.s0 = nw.s1 = 0;
-    if (tn >= P.ntiles) return;
-    const TileMeta m = P.tiles[tn];
-    nw.s0 = m.s0;
-    nw.s1 = m.s1;
-    if (P.pf & 1) {
+__device__ __forceinline__ void fetch_tile(const DevPlan &P, int32_t t, TileCache &tc) {
+    tc.nw = 0;
+    if (t >= P.ntiles) {
+        tc.m.s0 = tc.m.s1 = 0;
+        return;
+    }
+    const TileMeta m = P.tiles[t];
+    tc.m = m;
+    if (P.pf & 1) {  // the whole tile's records into L2
         const int64_t o0 = __ldg(P.slice_off + m.s0), o1 = __ldg(P.slice_off + m.s1);
         for (int64_t o = o0; o < o1; o += 4096)  // 64 KB per bulk prefetch
             bulk_prefetch_l2(P.rec + o * 16, (uint32_t)((o1 - o < 4096 ? o1 - o : 4096) * 16));
     }
     if (m.u0 >= 0) return;
-    nw.n = m.w1 - m.w0;
-    for (int w = 0; w < nw.n; w++) {
-        nw.lo[w] = __ldg(&P.wins[m.w0 + w].lo);
-        nw.len[w] = __ldg(&P.wins[m.w0 + w].len);
-        nw.off[w] = __ldg(&P.wins[m.w0 + w].loff);
+    tc.nw = m.w1 - m.w0;
+    for (int w = 0; w < tc.nw; w++) {
+        tc.lo[w] = __ldg(&P.wins[m.w0 + w].lo);
+        tc.len[w] = __ldg(&P.wins[m.w0 + w].len);
+        tc.off[w] = __ldg(&P.wins[m.w0 + w].loff);
     }
 }
 
-__device__ __forceinline__ void issue_x_cached(const double *x, const NextWins &nw, double *xs,
+// Issue the even-aligned x windows of a cached tile into xs with TMA bulk
+// copies; every tile arrives once on xbar (list-mode and past-the-end tiles
+// with 0 bytes) so the barrier's phases count tiles.
+__device__ __forceinline__ void issue_x_cached(const double *x, const TileCache &tc, double *xs,
                                               uint64_t *xbar) {
     uint32_t bytes = 0;
-    for (int w = 0; w < nw.n; w++)
-        if (tma_window(nw.lo[w], nw.len[w])) bytes += (uint32_t)nw.len[w] * 8;
+    for (int w = 0; w < tc.nw; w++)
+        if (tma_window(tc.lo[w], tc.len[w])) bytes += (uint32_t)tc.len[w] * 8;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_tx(xbar, bytes);
-    for (int w = 0; w < nw.n; w++)
-        if (tma_window(nw.lo[w], nw.len[w]))
-            bulk_load(xs + nw.off[w], x + nw.lo[w], (uint32_t)nw.len[w] * 8, xbar);
+    for (int w = 0; w < tc.nw; w++)
+        if (tma_window(tc.lo[w], tc.len[w]))
+            bulk_load(xs + tc.off[w], x + tc.lo[w], (uint32_t)tc.len[w] * 8, xbar);
+}
+
+// record offsets of a tile's slices into shared memory (LDGSTS, one group)
+__device__ __forceinline__ void load_offsets(const DevPlan &P, const TileMeta &m, int64_t *dst,
+                                             int tid) {
+    const int nn = m.s1 - m.s0;
+    for (int i = tid; i <= nn && nn > 0; i += kThreads)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr(dst + i)),
+                     "l"(P.slice_off + m.s0 + i)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 // ---- fixed-point accumulation ---------------------------------------------
@@ -316,10 +307,10 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
     uint32_t *wmid = wlo + S;  // two-word mode: the high word
     uint32_t *whi = wmid + S;
     __shared__ int64_t s_off[2][kMaxTileSlices + 1];
-    __shared__ int32_t s_t[2];
+    __shared__ int32_t s_t[3];  // tiles k, k+1 (known) and k+2 (claimed during tile k)
     __shared__ int32_t s_ex[2];
     __shared__ __align__(8) uint64_t xbar;
-    __shared__ NextWins s_next;
+    __shared__ TileCache s_tc[2];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int i = tid; i < S; i += kThreads) {
         xs[i] = 0.0;  // the sink's x stays 0
@@ -331,17 +322,19 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
             acc[i] = 0.0;
         }
     }
-    if (tid == 0) {
-        mbar_init(&xbar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s_t[0] = atomicAdd(P.counter, 1);
-        s_ex[0] = s_ex[1] = -1100;
-        s_next.n = s_next.s0 = s_next.s1 = 0;  // read (racily, prefetch hints only) before the first fetch_next
-    }
     // PARS3_PHASES=1: thread 0 accumulates SM cycles per phase
     // (totals in shared memory: no registers held across the tile loop)
     __shared__ long long s_clk[6];
     if (tid < 6) s_clk[tid] = 0;
+    if (tid == 0) {
+        mbar_init(&xbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_t[0] = atomicAdd(P.counter, 1);
+        s_t[1] = atomicAdd(P.counter, 1);
+        s_ex[0] = s_ex[1] = -1100;
+        fetch_tile(P, s_t[0], s_tc[0]);
+        issue_x_cached(x, s_tc[0], xs, &xbar);
+    }
     long long tprev = clock64();
 #define PHASE(k)                                  \
     do {                                          \
@@ -352,44 +345,37 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
         }                                         \
     } while (0)
     __syncthreads();
-    {
-        const int32_t t0 = s_t[0];
-        if (t0 < P.ntiles) {
-            const int s0 = __ldg(&P.tiles[t0].s0), n0 = __ldg(&P.tiles[t0].s1) - s0;
-            for (int i = tid; i <= n0; i += kThreads) s_off[0][i] = __ldg(P.slice_off + s0 + i);
-        }
-        if (tid == 0) issue_x(P, x, t0, xs, &xbar);
-    }
+    load_offsets(P, s_tc[0].m, s_off[0], tid);
 
     for (int k = 0;; k++) {
         const int cur = k & 1, nxt = cur ^ 1;
-        const int32_t t = s_t[cur];
+        const int32_t t = s_t[k % 3];
         if (t >= P.ntiles) break;
-        const TileMeta m = P.tiles[t];
-        const int nown = m.r1 - m.r0;
-        const int nsl = m.s1 - m.s0;
-        if (tid == 0) s_t[nxt] = atomicAdd(P.counter, 1);  // claim the next tile ahead
+        const TileCache &tc = s_tc[cur];
+        const int32_t r0 = tc.m.r0, r1 = tc.m.r1, u0 = tc.m.u0, local = tc.m.local;
+        const int nsl = tc.m.s1 - tc.m.s0;
+        // claim tile k+2 now; the atomic's latency hides behind this tile
+        int32_t claimed = 0;
+        if (tid == 0) claimed = atomicAdd(P.counter, 1);
         PHASE(0);
 
-        // 1. x over the tile's local slots: windows arrived by TMA (issued at
-        //    the end of the previous tile), odd-aligned windows and list-mode
-        //    slots loaded here
-        if (m.u0 >= 0) {
-            const int32_t *uc = P.ucol + m.u0;
-            for (int i = tid; i < m.local; i += kThreads) xs[i] = __ldg(x + __ldg(uc + i));
+        // 1. x over the tile's local slots: windows arrived by TMA (issued
+        //    during the previous tile's flush), odd-aligned windows and
+        //    list-mode slots gathered here
+        if (u0 >= 0) {
+            const int32_t *uc = P.ucol + u0;
+            for (int i = tid; i < local; i += kThreads) xs[i] = __ldg(x + __ldg(uc + i));
         } else {
-            for (int w = m.w0; w < m.w1; w++) {
-                const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
-                          off = __ldg(&P.wins[w].loff);
-                if (!tma_window(lo, len))
-                    for (int i = tid; i < len; i += kThreads) xs[off + i] = __ldg(x + lo + i);
-            }
+            for (int w = 0; w < tc.nw; w++)
+                if (!tma_window(tc.lo[w], tc.len[w]))
+                    for (int i = tid; i < tc.len[w]; i += kThreads)
+                        xs[tc.off[w] + i] = __ldg(x + tc.lo[w] + i);
         }
         mbar_wait(&xbar, (uint32_t)(k & 1), P.watchdog, 5, t);
         asm volatile("cp.async.wait_all;" ::: "memory");  // this tile's record offsets
         if (kFixed) {  // tile-wide bound on |x|: max binary exponent over the slots
             int e = -1100;
-            for (int i = tid; i < m.local; i += kThreads) {
+            for (int i = tid; i < local; i += kThreads) {
                 const int be = (int)((__double_as_longlong(xs[i]) >> 52) & 0x7FF);
                 e = max(e, be - 1022);  // |x| < 2^(be - 1022) for normal x
             }
@@ -399,13 +385,13 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
         __syncthreads();
         PHASE(1);
         if (tid == 0) {
-            fetch_next(P, s_t[nxt], s_next);  // overlaps the stream
+            fetch_tile(P, s_t[(k + 1) % 3], s_tc[nxt]);  // overlaps the stream
             s_ex[nxt] = -1100;
         }
         int E = 0;
         double scale = 0.0, unscale = 0.0;
         if (kFixed) {
-            E = m.ev + s_ex[cur] + 3;
+            E = tc.m.ev + s_ex[cur] + 3;
             E = max(-1000, min(1000, E));
             scale = ldexp(1.0, 50 - E);
             unscale = ldexp(1.0, E - 50);
@@ -436,16 +422,16 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
                 }
             }
             const double xr = xs[rl];
-            double r0 = 0.0, r1 = 0.0;  // two chains: even and odd slots
+            double c0 = 0.0, c1 = 0.0;  // two row-sum chains: even and odd slots
             if (kFixed) {
                 const double nxs = -xr * scale;  // mirror term v * (-x_r), scaled
 #pragma unroll
                 for (int u = 0; u < kMaxSlots; u++) {
                     if (u < ns) {
                         if (u & 1)
-                            r1 = fma(v[u], xs[li[u]], r1);
+                            c1 = fma(v[u], xs[li[u]], c1);
                         else
-                            r0 = fma(v[u], xs[li[u]], r0);
+                            c0 = fma(v[u], xs[li[u]], c0);
                         const double q = fma(v[u], nxs, kMagic);
                         if (kWords == 3)
                             fx_add3m<S>(wlo, li[u], q);
@@ -453,7 +439,7 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
                             fx_add2m<S>(wlo, li[u], q);
                     }
                 }
-                const double q = fma(r0 + r1, scale, kMagic);
+                const double q = fma(c0 + c1, scale, kMagic);
                 if (kWords == 3)
                     fx_add3m<S>(wlo, rl, q);
                 else
@@ -463,29 +449,39 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
                 for (int u = 0; u < kMaxSlots; u++) {
                     if (u < ns) {
                         if (u & 1)
-                            r1 = fma(v[u], xs[li[u]], r1);
+                            c1 = fma(v[u], xs[li[u]], c1);
                         else
-                            r0 = fma(v[u], xs[li[u]], r0);
+                            c0 = fma(v[u], xs[li[u]], c0);
                         atomicAdd(&acc[li[u]], -v[u] * xr);
                     }
                 }
-                atomicAdd(&acc[rl], r0 + r1);
+                atomicAdd(&acc[rl], c0 + c1);
             }
         }
-        if ((P.pf & 4) && lane == 0) {  // warm L2 with the next tile's first slices
-            const int sn = s_next.s0 + warp * P.pf_dist;
-            for (int q = 0; q < P.pf_dist && sn + q < s_next.s1; q++) {
-                const int64_t a = __ldg(P.slice_off + sn + q), b = __ldg(P.slice_off + sn + q + 1);
-                bulk_prefetch_l2(P.rec + a * 16, (uint32_t)((b - a) * 16));
+        if (tid == 0) {
+            s_t[(k + 2) % 3] = claimed;
+            if (P.pf & 4) {  // warm L2 with the next tile's first slices
+                const TileMeta &mn = s_tc[nxt].m;
+                const int q1 = min(mn.s1, mn.s0 + kWarps * P.pf_dist);
+                if (q1 > mn.s0) {
+                    const int64_t a = __ldg(P.slice_off + mn.s0), b = __ldg(P.slice_off + q1);
+                    bulk_prefetch_l2(P.rec + a * 16, (uint32_t)((b - a) * 16));
+                }
             }
         }
         __syncthreads();
         PHASE(2);
 
-        // 3. deliver: every slot's value (own rows + diag * x) reduces into y
-        //    with a fire-and-forget fp64 red (consecutive slots -> coalesced
-        //    L2 reductions); the accumulators are cleared in the same pass
-        const int32_t tn = s_t[nxt];
+        // 3. xs is free: the next tile's x windows and record offsets are
+        //    issued first, so they land while this tile flushes
+        if (tid == 0) issue_x_cached(x, s_tc[nxt], xs, &xbar);
+        load_offsets(P, s_tc[nxt].m, s_off[nxt], tid);
+        PHASE(4);
+
+        // 4. deliver: every slot's value (own rows + diag * x, x of own rows
+        //    from global: xs already holds the next tile) reduces into y with
+        //    a fire-and-forget fp64 red (consecutive slots -> coalesced L2
+        //    reductions); the accumulators are cleared in the same pass
         auto take = [&](int i) -> double {
             if (kWords == 3) {
                 const double a = fx_value(wlo[i], wmid[i], whi[i], unscale);
@@ -501,41 +497,30 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
             acc[i] = 0.0;
             return a;
         };
-        if (m.u0 >= 0) {
-            const int32_t *uc = P.ucol + m.u0;
-            const int nmsg = m.local - nown;  // own rows are the tail of the list
-            for (int i = tid; i < m.local; i += kThreads) {
+        if (u0 >= 0) {
+            const int32_t *uc = P.ucol + u0;
+            const int nmsg = local - (r1 - r0);  // own rows are the tail of the list
+            for (int i = tid; i < local; i += kThreads) {
                 double a = take(i);
+                const int c = __ldg(uc + i);
                 if (i >= nmsg)
-                    a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + m.r0 + (i - nmsg)), xs[i], a);
-                if (a != 0.0) atomicAdd(y + __ldg(uc + i), a);
+                    a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), __ldg(x + c), a);
+                if (a != 0.0) atomicAdd(y + c, a);
             }
         } else {
-            for (int w = m.w0; w < m.w1; w++) {
-                const int lo = __ldg(&P.wins[w].lo), len = __ldg(&P.wins[w].len),
-                          off = __ldg(&P.wins[w].loff);
+            for (int w = 0; w < tc.nw; w++) {
+                const int lo = tc.lo[w], len = tc.len[w], off = tc.off[w];
                 for (int i = tid; i < len; i += kThreads) {
                     const int c = lo + i;
                     double a = take(off + i);
-                    if (c >= m.r0 && c < m.r1)
-                        a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), xs[off + i], a);
+                    if (c >= r0 && c < r1)
+                        a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), __ldg(x + c), a);
                     if (a != 0.0) atomicAdd(y + c, a);
                 }
             }
         }
         __syncthreads();
         PHASE(3);
-        // 4. the next tile: x windows into the now-free xs, record offsets
-        if (tid == 0) issue_x_cached(x, s_next, xs, &xbar);
-        if (tn < P.ntiles) {  // async copies (LDGSTS): waited for before the next stream
-            const int s0n = s_next.s0, nn = s_next.s1 - s0n;
-            for (int i = tid; i <= nn; i += kThreads)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr(&s_off[nxt][i])),
-                             "l"(P.slice_off + s0n + i)
-                             : "memory");
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        }
-        PHASE(4);
     }
     if (P.phase_clk && tid == 0)
         for (int k = 0; k < 6; k++) atomicAdd(P.phase_clk + k, (unsigned long long)s_clk[k]);
