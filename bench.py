@@ -245,10 +245,11 @@ def run_gpu(args):
         stats = op.stats()
     else:
         from paper_2407_17651_b200.distributed import DistributedPars3
-        dop = DistributedPars3(s, plan)
-        op = dop._op
-        launches_per_step = op.kernel_count(with_dot=False) + 1
+        dop = DistributedPars3(s, plan, max_ctas=int(os.environ.get("PARS3_MAX_CTAS", "0")))
+        op = dop._op  # the interior product (dominant kernel)
+        launches_per_step = sum(o.kernel_count(with_dot=False) for o in dop.ops) + 1  # + k_dot
         stats = op.stats()
+        stats["boundary_entries"] = dop.ops[1].stats()["entries"] if len(dop.ops) > 1 else 0
     torch.cuda.synchronize()
     log(f"rank {rank}: rows [{lo}, {hi}) device plan {time.time() - t0:.1f}s {stats}")
     x = torch.from_numpy(x_host[lo:hi].copy()).cuda()
@@ -260,8 +261,8 @@ def run_gpu(args):
             y, d = op.matvec_dot(x, None, y=ybuf, dot=dot)
             return y
         y = dop.matvec(x)
-        d = torch.dot(y, y).reshape(1)
-        dist.all_reduce(d)
+        P.device.dot(y, y, out=dot)
+        dist.all_reduce(dot)
         return y
 
     ybuf = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
@@ -308,13 +309,17 @@ def run_gpu(args):
         barrier()
     step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
 
-    # dominant kernel: the local SpMV alone, same clock discipline
+    # dominant kernel: the local SpMV alone (every local part at N > 1), same
+    # clock discipline
     xk = dop.x_ext if dist is not None else x
     yk = dop.y_ext if dist is not None else ybuf
+    local_ops = dop.ops if dist is not None else [op]
     barrier()
     ev0.record()
     for _ in range(args.steps):
-        op.matvec(xk, yk)
+        local_ops[0].matvec(xk, yk)
+        for o in local_ops[1:]:
+            o.matvec(xk, yk, accumulate=True)
     ev1.record()
     barrier()
     spmv_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
@@ -350,7 +355,7 @@ def run_gpu(args):
     peak, peak_src = peak_hbm()
     value = B / (step_ms * 1e-3) / 1e9
     # per-GPU kernel roofline: this rank's share of the algorithmic bytes
-    own_nnz = int(stats["entries"])
+    own_nnz = int(stats["entries"]) + int(stats.get("boundary_entries", 0))
     B_rank = algorithmic_bytes(hi - lo, own_nnz) if world > 1 else B
     achieved = B_rank / (spmv_ms * 1e-3) / 1e9
     traffic = None

@@ -75,8 +75,16 @@ typedef struct pars3_plan_options {
     int32_t seg_max;      /* max entries per row segment (<= 8) */
     int32_t gap;          /* merge column runs separated by <= gap slots (8); -1 = default */
     int32_t mode;         /* accumulation of the mirror sums: 0 auto, 1 exact-integer fixed
-                             point (3 x 32-bit words), 2 fp64 shared-memory atomics */
+                             point (3 x 32-bit words), 2 fp64 shared-memory atomics, 3
+                             exact-integer fixed point (2 words, <= 64 terms per slot) */
+    int32_t flags;        /* PARS3_PLAN_SKIP_EMPTY: rows without stored entries get no slot
+                             (their diagonal term is dropped: for partial plans whose
+                             diagonal lives in another plan) */
+    int32_t max_ctas;     /* cap on the persistent grid (0 = every resident CTA); leaves
+                             SMs free for a concurrent exchange (multi-GPU overlap) */
 } pars3_plan_options;
+
+#define PARS3_PLAN_SKIP_EMPTY 1
 
 /* Build the device plan of a split on the current device: replaces the
  * per-call setup of _pars3 (parallel.py:136-183).  The split's diagonal,
@@ -92,11 +100,20 @@ int pars3_plan_create(const pars3_split_view *split, const pars3_plan_options *o
  * spmv_pars3 parallel.py:136-183).  y is overwritten. */
 int pars3_plan_spmv(pars3_plan *plan, const double *x, double *y, void *stream);
 
+/* y += A x through a plan (y is NOT zeroed): several plans over the same
+ * index space (e.g. a rank's interior and boundary rows, DistributedPars3)
+ * accumulate into one y. */
+int pars3_plan_spmv_acc(pars3_plan *plan, const double *x, double *y, void *stream);
+
 /* y = A x and *dot = <y, w> in one pass (MRS-style step; no reference
  * counterpart: the reference stops at the product).  `dot` is
  * a device pointer to one double; w may equal x. */
 int pars3_plan_spmv_dot(pars3_plan *plan, const double *x, double *y, const double *w,
                         double *dot, void *stream);
+
+/* *out = <a, b> over n doubles (device pointers, 16-byte aligned): the
+ * inner product of a distributed MRS step before its all-reduce. */
+int pars3_dot(int64_t n, const double *a, const double *b, double *out, void *stream);
 
 /* Number of libpars3 kernels one pars3_plan_spmv (with_dot = 0) or
  * pars3_plan_spmv_dot (with_dot = 1) call launches (memsets excluded). */
@@ -106,16 +123,13 @@ int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *c
 int pars3_plan_bytes(const pars3_plan *plan, int64_t *bytes);
 
 /* stats[10] = {tiles, slices, padded slots, stored entries, windows,
- * max local slots, grid CTAs, device bytes, list-mode tiles, accumulate}. */
+ * max local slots, grid CTAs, device bytes, list-mode tiles, accumulator
+ * words (0 = fp64, 2 or 3 = fixed point)}. */
 int pars3_plan_stats(const pars3_plan *plan, int64_t *stats);
 int pars3_plan_destroy(pars3_plan *plan);
 
-/* Debug: host address of the plan's progress-trace buffer (mapped host
- * memory, 32 int32 per CTA) when created with PARS3_TRACE=1, else NULL. */
-int pars3_plan_trace(const pars3_plan *plan, int32_t **host);
-
-/* Debug: per-phase SM-cycle totals of the tile kernel (created with
- * PARS3_PHASES=1; claim, windows, stream, store, wait, flush). */
+/* Debug: per-phase SM-cycle totals of the tile kernel's thread 0 (plan
+ * created with PARS3_PHASES=1): claim, windows, stream, flush, issue-next, -. */
 int pars3_plan_phases(const pars3_plan *plan, int64_t *out6);
 
 /* ------------------------------------------------ MRS iteration kernels */

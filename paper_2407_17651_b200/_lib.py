@@ -41,7 +41,10 @@ class PlanOptions(ctypes.Structure):
     """Mirror of ``pars3_plan_options``."""
 
     _fields_ = [("tile_rows", _c_i32), ("local_slots", _c_i32), ("seg_max", _c_i32),
-                ("gap", _c_i32), ("mode", _c_i32)]
+                ("gap", _c_i32), ("mode", _c_i32), ("flags", _c_i32), ("max_ctas", _c_i32)]
+
+
+PLAN_SKIP_EMPTY = 1
 
 
 # name -> (restype, argtypes)
@@ -52,12 +55,13 @@ _SIGS = {
     "pars3_plan_create": (ctypes.c_int, [ctypes.POINTER(SplitView), ctypes.POINTER(PlanOptions),
                                          _c_i32, _vp, ctypes.POINTER(_vp), _vp]),
     "pars3_plan_spmv": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "pars3_plan_spmv_acc": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "pars3_plan_spmv_dot": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_plan_bytes": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i64)]),
+    "pars3_dot": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
     "pars3_plan_stats": (ctypes.c_int, [_vp, _vp]),
     "pars3_plan_kernel_count": (ctypes.c_int, [_vp, _c_i32, ctypes.POINTER(_c_i32)]),
     "pars3_plan_destroy": (ctypes.c_int, [_vp]),
-    "pars3_plan_trace": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     "pars3_plan_phases": (ctypes.c_int, [_vp, _vp]),
     "pars3_mrs_lanczos": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, ctypes.c_double, ctypes.c_double,
                                          _vp, _vp]),

@@ -91,9 +91,11 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
                  std::vector<Draft> &out, std::vector<int32_t> &scratch) {
     scratch.clear();
     int64_t segments = 0;
+    int64_t entries = 0;
     for (int32_t r = a; r < b; r++) {
-        scratch.push_back(r);
         int64_t c = R.count(r);
+        entries += c;
+        if (c > 0 || !o.skip_empty) scratch.push_back(r);
         segments += (c + o.seg_max - 1) / o.seg_max;
         for (int64_t k = 0; k < c; k++) scratch.push_back(R.col(r, k));
     }
@@ -103,6 +105,7 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
         draft_range(R, mid, b, o, out, scratch);
         return;
     }
+    if (entries == 0 && o.skip_empty) return;  // nothing to deliver
     Draft d;
     d.r0 = a;
     d.r1 = b;
@@ -159,7 +162,7 @@ void materialise(const Rows &R, const Draft &d, const PlanOptions &o, Built &b) 
     b.r0 = d.r0;
     b.r1 = d.r1;
     b.local = d.local;
-    b.own_loff = local_of(d, b.wloff, d.r0);
+    b.own_loff = (!d.wlo.empty() && d.r0 >= d.wlo[0]) ? local_of(d, b.wloff, d.r0) : 0;
     b.list = (int)d.wlo.size() > kMaxWindows || d.hub >= 0;
     if (b.list) {
         b.ucol.reserve(d.local);

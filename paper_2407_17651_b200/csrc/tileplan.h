@@ -29,6 +29,7 @@ struct PlanOptions {
     int32_t mode = 0;           // accumulation: 0 auto, 1 fixed point (3 words), 2 fp64,
                                 // 3 fixed point (2 words) (tiles.cu)
     uint16_t sink = kNoSlot;    // local slot that padding lanes / entries point at (> local_slots)
+    bool skip_empty = false;    // rows without entries get no own slot (no diagonal term)
 };
 
 constexpr int kMaxWindows = 8;  // more windows than this -> explicit column list

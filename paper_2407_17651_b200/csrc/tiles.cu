@@ -1,23 +1,24 @@
-// Windowed tile kernel: the single-GPU PARS3 product.
+// Windowed tile kernel: the PARS3 product y = A x on one GPU (DESIGN.md
+// section 3).
 //
-// One persistent CTA per SM; tiles are claimed in ascending order from an
-// atomic counter.  Per tile:
-//   1. the tile's column windows of x are copied into shared memory (xs) and
-//      the matching accumulators (acc) zeroed;
-//   2. each warp streams its SELL-32 slice records (fp64 value + uint16 local
-//      column) through a private TMA ring (cp.async.bulk + mbarrier):
-//      lane l owns one row segment, keeps its row sum in a register
-//      (+a_ic * x_c, serial.py:56-57) and adds the mirror -a_ic * x_i into
-//      acc[c] (serial.py:58-59) -- both in shared memory, no global atomics;
-//   3. the tile's own rows are final except for contributions of LATER
-//      tiles: y[r] = diag_r x_r + acc[r] is stored, then the tile's flag is
-//      released (this is the reference's "owner" write, parallel.py:85-95);
-//   4. the remaining window slots (columns below the tile) are this tile's
-//      accumulation messages (the reference's msg_val / MPI_Accumulate,
-//      parallel.py:96-113): after the owning tiles have
-//      released their flags they are added into y with fp64 reductions.
-// Waits only ever target lower tile indices, which were claimed earlier by
-// running CTAs that never wait before releasing, so the loop cannot deadlock.
+// A persistent grid (4 CTAs x 8 warps per SM) claims row tiles in ascending
+// order from an atomic counter, two tiles ahead.  Per tile:
+//   1. x over the tile's local index space is in shared memory (xs): dense
+//      column windows arrive by TMA bulk copies issued during the previous
+//      tile's flush; list-mode tiles gather their explicit column list;
+//   2. each warp streams SELL-32 slice records (fp64 value + uint16 local
+//      column) straight into registers, with the next slice bulk-prefetched
+//      into L2: lane l owns one row segment, keeps its row sum in registers
+//      (+a_ic * x_c, serial.py:56-57) and adds the mirror -a_ic * x_i
+//      (serial.py:58-59) into the tile's shared accumulator of column c --
+//      exact-integer fixed point with native 32-bit shared atomics (or fp64);
+//   3. every slot's accumulated value (+ diag * x for the tile's own rows)
+//      is reduced into y with fire-and-forget fp64 L2 reductions: for own
+//      rows this is the reference's owner write (parallel.py:85-95), for
+//      columns below the tile the accumulation message (msg_val /
+//      MPI_Accumulate, parallel.py:96-113).
+// y is zeroed on the stream first (pars3_plan_spmv) or accumulated into
+// (pars3_plan_spmv_acc).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -37,10 +38,8 @@ using pars3::Window;
 
 namespace {
 
-constexpr uint16_t kNo = pars3::kNoSlot;
-// 2 CTAs per SM x 16 warps: the slice loop streams whole records into
-// registers (tools/microbench/mb3.cu: this inner loop alone runs at ~6.7 TB/s
-// on c5-shaped data), and the second CTA overlaps each CTA's per-tile
+// 4 CTAs per SM x 8 warps (<= 64 registers): 32 warps stream records into
+// registers, and the co-resident CTAs overlap each other's per-tile
 // window/flush phases.
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -70,29 +69,17 @@ struct DevPlan {
     const uint8_t *rec;
     const int32_t *ucol;
     const double *diag;
-    int32_t *flags;
     int32_t *counter;
     int32_t ntiles;
-    int32_t lmax;
-    int32_t stage_bytes;
-    int32_t accumulate;
     int32_t watchdog;
     int32_t diag_const;  // 1: every diagonal value equals diag_alpha (strict / shifted skew)
     double diag_alpha;
-    volatile int32_t *trace;  // mapped host memory, 32 ints per CTA (debug), or null
     unsigned long long *phase_clk;  // PARS3_PHASES=1: per-phase SM cycles (thread 0 of each CTA)
-    int32_t pf;  // L2 prefetch of records: bit 0 the next tile's records (claim time), bit 1 each
-                 // warp's slice pf_dist iterations ahead, bit 2 the next tile's first slices
-                 // when a warp leaves the stream
+    int32_t pf;  // L2 prefetch of records: bit 0 each tile's records when its metadata is
+                 // fetched, bit 1 each warp's slice pf_dist iterations ahead, bit 2 the
+                 // next tile's first slices at the end of the stream
     int32_t pf_dist;
 };
-
-// debug trace (PARS3_TRACE=1): progress markers readable by the host while the
-// kernel runs; slot 0-3 producer, 4-7 consumer leader, 8+ consumer warps
-#define TRACE(P, slot, v)                                                  \
-    do {                                                                   \
-        if ((P).trace) (P).trace[blockIdx.x * 32 + (slot)] = (int32_t)(v); \
-    } while (0)
 
 __device__ __forceinline__ uint32_t saddr(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -146,35 +133,6 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
         "l"(src), "r"(bytes), "r"(saddr(bar))
         : "memory");
 }
-__device__ __forceinline__ int32_t ld_acquire(const int32_t *p) {
-    int32_t v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release(int32_t *p, int32_t v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Spin until tile u's flag shows this launch's epoch.  With `watchdog` set
-// (PARS3_WATCHDOG=1) a wait that exceeds ~2^26 polls reports and gives up
-// instead of hanging the device (debug aid; results are then invalid).
-__device__ __forceinline__ void wait_flag(const int32_t *flags, int u, int32_t epoch, int t,
-                                          int watchdog) {
-    if (!watchdog) {
-        while (ld_acquire(flags + u) != epoch) {
-        }
-        return;
-    }
-    for (long long it = 0; ld_acquire(flags + u) != epoch; it++) {
-        if (it == (1ll << 26)) {
-            printf("pars3 watchdog: tile %d waits on tile %d (flag %d, epoch %d)\n", t, u,
-                   ld_acquire(flags + u), epoch);
-            return;
-        }
-    }
-}
-
 // TMA bulk prefetch of [p, p + bytes) into L2 (no shared memory, no registers):
 // keeps DRAM busy across a CTA's per-tile window/flush phases
 __device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
@@ -182,12 +140,6 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) 
 }
 
 __device__ __forceinline__ bool tma_window(int lo, int len) { return ((lo | len) & 1) == 0; }
-
-__device__ __forceinline__ void bulk_reduce_add(double *g, const double *s, uint32_t bytes) {
-    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(g),
-                 "r"(saddr(s)), "r"(bytes)
-                 : "memory");
-}
 
 // One tile's metadata and x-window list, copied into shared memory by
 // thread 0 one tile ahead (while the previous tile streams), so neither the
@@ -295,7 +247,7 @@ __device__ __forceinline__ double fx_value2(uint32_t lo, uint32_t hi, double uns
 // exact-integer fixed point in two / three 32-bit words per slot
 template <int kWords>
 __global__ void __launch_bounds__(kThreads, 4)
-k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t epoch) {
+k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
     constexpr bool kFixed = kWords > 0;
     constexpr int S = Layout<kWords>::kStride;
     constexpr uint32_t kSink = Layout<kWords>::kSink;
@@ -525,7 +477,6 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, int32_t
     if (P.phase_clk && tid == 0)
         for (int k = 0; k < 6; k++) atomicAdd(P.phase_clk + k, (unsigned long long)s_clk[k]);
 #undef PHASE
-    (void)epoch;
 }
 
 // <a, b>: 16-byte loads, four in flight per thread, one fp64 atomic per block
@@ -579,7 +530,6 @@ struct pars3_plan {
     int32_t p = 1;
     int32_t ntiles = 0, nslices = 0, lmax = 0;
     int64_t nnz = 0, slots = 0, nwins = 0;
-    int32_t epoch = 0;
     int grid = 0;
     size_t smem = 0;
     TileMeta *tiles = nullptr;
@@ -587,18 +537,15 @@ struct pars3_plan {
     int64_t *slice_off = nullptr;
     uint8_t *rec = nullptr;
     int32_t *ucol = nullptr;
-    int32_t stage_bytes = 0;
     double *diag = nullptr;
-    int32_t accumulate = 0, list_tiles = 0, watchdog = 0, diag_const = 0, words = 0, pf = 0, pf_dist = 1;
+    int32_t list_tiles = 0, watchdog = 0, diag_const = 0, words = 0, pf = 0, pf_dist = 1;
     double diag_alpha = 0.0;
-    int32_t *trace_host = nullptr, *trace_dev = nullptr;
     unsigned long long *phase_clk = nullptr;
-    int32_t *flags = nullptr;
     int32_t *counter = nullptr;
     int64_t bytes = 0;
 
     ~pars3_plan() {
-        void *ptrs[] = {tiles, wins, slice_off, rec, ucol, diag, flags, counter};
+        void *ptrs[] = {tiles, wins, slice_off, rec, ucol, diag, counter, phase_clk};
         for (void *q : ptrs)
             if (q) cudaFree(q);
     }
@@ -614,12 +561,15 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     if (s->n < 0 || s->n >= INT32_MAX || s->beta < 1) PARS3_FAIL(PARS3_ERR_ARG, "bad split header");
     if (p < 1) PARS3_FAIL(PARS3_ERR_ARG, "worker count must be at least 1, got %d", p);
     PlanOptions o;
+    int32_t max_ctas = 0;
     if (opt) {
         if (opt->tile_rows > 0) o.tile_rows = opt->tile_rows;
         if (opt->local_slots > 0) o.local_slots = opt->local_slots;
         if (opt->seg_max > 0) o.seg_max = opt->seg_max;
         if (opt->gap >= 0) o.gap = opt->gap;
         if (opt->mode > 0) o.mode = opt->mode;
+        o.skip_empty = (opt->flags & PARS3_PLAN_SKIP_EMPTY) != 0;
+        if (opt->max_ctas > 0) max_ctas = opt->max_ctas;
     }
     // accumulation of the mirror sums: mode 2 = fp64 shared accumulators,
     // mode 1 = exact-integer fixed point in three words, mode 3 = two words
@@ -658,15 +608,13 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     pl->p = p;
     pl->ntiles = (int32_t)hp.tiles.size();
     pl->nslices = (int32_t)hp.slice_off.size() - 1;
-    pl->lmax = hp.max_local > 0 ? hp.max_local : 1;
-    pl->lmax = (pl->lmax + 1) & ~1;  // keep the accumulator array 16-byte aligned
+    pl->lmax = hp.max_local;
     pl->nnz = hp.nnz;
     pl->slots = hp.slots;
-    pl->stage_bytes = 64 + 320 * (hp.max_nslots > 0 ? hp.max_nslots : 1);
     pl->nwins = (int64_t)hp.wins.size();
     pl->list_tiles = hp.list_tiles;
     pl->words = words;
-    {
+    {  // tuning and debug knobs (environment)
         const char *wd = getenv("PARS3_WATCHDOG");
         pl->watchdog = (wd && wd[0] == '1') ? 1 : 0;
         const char *pf = getenv("PARS3_PF");
@@ -678,28 +626,12 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
             cudaMalloc((void **)&pl->phase_clk, 8 * sizeof(unsigned long long));
             cudaMemset(pl->phase_clk, 0, 8 * sizeof(unsigned long long));
         }
-        const char *tr = getenv("PARS3_TRACE");
-        if (tr && tr[0] == '1') {
-            if (cudaHostAlloc((void **)&pl->trace_host, 32 * 4096 * sizeof(int32_t),
-                              cudaHostAllocMapped) == cudaSuccess) {
-                memset(pl->trace_host, 0xff, 32 * 4096 * sizeof(int32_t));
-                cudaHostGetDevicePointer((void **)&pl->trace_dev, pl->trace_host, 0);
-            }
-        }
     }
-    // accumulate mode (y zeroed, every contribution a reduction) when y is
-    // L2-sized or the matrix is unstructured; ordered mode (owner stores,
-    // later tiles reduce after the owner's flag) otherwise -- DESIGN.md
-    if (const char *md = getenv("PARS3_MODE")) o.mode = atoi(md);  // debug override
-    // the kernel accumulates every contribution into a zeroed y (the
-    // owner-stores-first "ordered" variant measured slower and was retired)
-    pl->accumulate = 1;
     std::vector<double> diag(s->diag, s->diag + s->n);
     pl->diag_const = 1;
     pl->diag_alpha = s->n ? diag[0] : 0.0;
     for (int64_t i = 1; i < s->n && pl->diag_const; i++)
         if (diag[i] != diag[0]) pl->diag_const = 0;
-    std::vector<int32_t> zeros(pl->ntiles + 1, 0);
 #define UP(dst, src)                               \
     do {                                           \
         int _r = upload(&pl->dst, src);            \
@@ -714,8 +646,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     UP(slice_off, hp.slice_off);
     UP(rec, hp.rec);
     UP(ucol, hp.ucol);
-    UP(diag, diag);
-    UP(flags, zeros);
+    if (!pl->diag_const) UP(diag, diag);
 #undef UP
     if (cudaMalloc((void **)&pl->counter, sizeof(int32_t)) != cudaSuccess) {
         delete pl;
@@ -723,7 +654,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     }
     pl->smem = pl->words == 0 ? Layout<0>::kSmem : pl->words == 2 ? Layout<2>::kSmem : Layout<3>::kSmem;
     // the attribute is per function, shared by every plan: set it to the
-    // largest window space any plan may use, not to this plan's size
+    // function's fixed layout size
     cudaError_t e = cudaFuncSetAttribute(k_tiles<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Layout<0>::kSmem);
     if (e == cudaSuccess)
@@ -745,42 +676,44 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
                    cudaGetErrorString(e));
     }
     pl->grid = per_sm * sms;
+    if (max_ctas > 0 && pl->grid > max_ctas) pl->grid = max_ctas;
     if (pl->grid > pl->ntiles) pl->grid = pl->ntiles > 0 ? pl->ntiles : 1;
     *out = pl;
     return PARS3_OK;
 }
 
-static int launch_tiles(pars3_plan *pl, const double *x, double *y, cudaStream_t st) {
+static int launch_tiles(pars3_plan *pl, const double *x, double *y, bool zero_y, cudaStream_t st) {
+    if (zero_y && pl->n > 0) CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)pl->n, st));
     if (pl->ntiles == 0) return PARS3_OK;
-    if (++pl->epoch == INT32_MAX) {  // wrap: clear the flags once every 2^31 products
-        pl->epoch = 1;
-        CUDA_TRY(cudaMemsetAsync(pl->flags, 0, sizeof(int32_t) * pl->ntiles, st));
-    }
     CUDA_TRY(cudaMemsetAsync(pl->counter, 0, sizeof(int32_t), st));
-    CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)pl->n, st));
-    DevPlan P{pl->tiles,   pl->wins,    pl->slice_off, pl->rec,  pl->ucol,        pl->diag,
-              pl->flags,   pl->counter, pl->ntiles,    pl->lmax, pl->stage_bytes, pl->accumulate,
-              pl->watchdog, pl->diag_const, pl->diag_alpha, pl->trace_dev, pl->phase_clk, pl->pf, pl->pf_dist};
+    DevPlan P{pl->tiles,      pl->wins,       pl->slice_off, pl->rec,       pl->ucol,
+              pl->diag,       pl->counter,    pl->ntiles,    pl->watchdog,  pl->diag_const,
+              pl->diag_alpha, pl->phase_clk,  pl->pf,        pl->pf_dist};
     if (pl->words == 0)
-        k_tiles<0><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
+        k_tiles<0><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
     else if (pl->words == 2)
-        k_tiles<2><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
+        k_tiles<2><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
     else
-        k_tiles<3><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, pl->epoch);
+        k_tiles<3><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
     LAUNCH_CHECK();
     return PARS3_OK;
 }
 
 extern "C" int pars3_plan_spmv(pars3_plan *pl, const double *x, double *y, void *stream) {
     if (!pl || (pl->n > 0 && (!x || !y))) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
-    return launch_tiles(pl, x, y, (cudaStream_t)stream);
+    return launch_tiles(pl, x, y, true, (cudaStream_t)stream);
+}
+
+extern "C" int pars3_plan_spmv_acc(pars3_plan *pl, const double *x, double *y, void *stream) {
+    if (!pl || (pl->n > 0 && (!x || !y))) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
+    return launch_tiles(pl, x, y, false, (cudaStream_t)stream);
 }
 
 extern "C" int pars3_plan_spmv_dot(pars3_plan *pl, const double *x, double *y, const double *w,
                                    double *dot, void *stream) {
     if (!pl || !dot || (pl->n > 0 && (!x || !y || !w))) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
     cudaStream_t st = (cudaStream_t)stream;
-    int rc = launch_tiles(pl, x, y, st);
+    int rc = launch_tiles(pl, x, y, true, st);
     if (rc) return rc;
     CUDA_TRY(cudaMemsetAsync(dot, 0, sizeof(double), st));
     if (pl->n > 0) {
@@ -789,6 +722,17 @@ extern "C" int pars3_plan_spmv_dot(pars3_plan *pl, const double *x, double *y, c
         k_dot<<<148 * 4, 512, 0, st>>>((int32_t)pl->n, y, w, dot);
         LAUNCH_CHECK();
     }
+    return PARS3_OK;
+}
+
+extern "C" int pars3_dot(int64_t n, const double *a, const double *b, double *out, void *stream) {
+    if (n < 0 || n >= INT32_MAX || !out || (n > 0 && (!a || !b))) PARS3_FAIL(PARS3_ERR_ARG, "bad argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
+    if (n == 0) return PARS3_OK;
+    if (((uintptr_t)a | (uintptr_t)b) & 15) PARS3_FAIL(PARS3_ERR_ARG, "a and b must be 16-byte aligned");
+    k_dot<<<148 * 4, 512, 0, st>>>((int32_t)n, a, b, out);
+    LAUNCH_CHECK();
     return PARS3_OK;
 }
 
@@ -825,13 +769,6 @@ extern "C" int pars3_plan_phases(const pars3_plan *pl, int64_t *out6) {
     unsigned long long h[8] = {0};
     if (pl->phase_clk) CUDA_TRY(cudaMemcpy(h, pl->phase_clk, sizeof(h), cudaMemcpyDeviceToHost));
     for (int k = 0; k < 6; k++) out6[k] = (int64_t)h[k];
-    return PARS3_OK;
-}
-
-// debug: host address of the trace buffer (PARS3_TRACE=1), else null
-extern "C" int pars3_plan_trace(const pars3_plan *pl, int32_t **host) {
-    if (!pl || !host) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
-    *host = pl->trace_host;
     return PARS3_OK;
 }
 

@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 
 __all__ = ["require_cuda", "Pars3Operator", "SssDevice", "operator_for_split", "operator_for_sss",
-           "sss_device"]
+           "sss_device", "dot"]
 
 
 def require_cuda():
@@ -56,7 +56,8 @@ class Pars3Operator:
                               _lib.ptr(host["mid_col"]), _lib.ptr(host["mid_val"]),
                               int(host["outer_col"].size), _lib.ptr(host["outer_row"]),
                               _lib.ptr(host["outer_col"]), _lib.ptr(host["outer_val"]))
-        opts = _lib.PlanOptions(*(tuple(options or ()) + (0, 0, 0, -1, 0)[len(options or ()):]))
+        # (tile_rows, local_slots, seg_max, gap, mode, flags, max_ctas); 0 / -1 = default
+        opts = _lib.PlanOptions(*(tuple(options or ()) + (0, 0, 0, -1, 0, 0, 0)[len(options or ()):]))
         bs = _c(block_start if block_start is not None else [0, self.n], np.int64)
         handle = ctypes.c_void_p()
         L = _lib.load()
@@ -68,12 +69,16 @@ class Pars3Operator:
         self._L = L
 
     # -- hot entry points (device tensors in, device tensors out) ---------
-    def matvec(self, x, y=None, stream=None):
-        """y = A x for a contiguous float64 CUDA tensor x of length n."""
+    def matvec(self, x, y=None, stream=None, accumulate=False):
+        """y = A x for a contiguous float64 CUDA tensor x of length n
+        (``accumulate``: y += A x, y not zeroed)."""
         if y is None:
             y = self.torch.empty(self.n, dtype=self.torch.float64, device=self.device)
-        _lib.check(self._L.pars3_plan_spmv(self._handle, _lib.ptr(x), _lib.ptr(y),
-                                           _lib.stream_ptr(stream)), "pars3_plan_spmv")
+            if accumulate:
+                y.zero_()
+        f = self._L.pars3_plan_spmv_acc if accumulate else self._L.pars3_plan_spmv
+        _lib.check(f(self._handle, _lib.ptr(x), _lib.ptr(y), _lib.stream_ptr(stream)),
+                   "pars3_plan_spmv")
         return y
 
     def matvec_dot(self, x, w, y=None, dot=None, stream=None):
@@ -117,6 +122,16 @@ class Pars3Operator:
             self.close()
         except Exception:
             pass
+
+
+def dot(a, b, out=None, stream=None):
+    """<a, b> of two float64 CUDA vectors into a device scalar (libpars3 k_dot)."""
+    torch = require_cuda()
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=a.device)
+    _lib.check(_lib.load().pars3_dot(a.numel(), _lib.ptr(a), _lib.ptr(b), _lib.ptr(out),
+                                     _lib.stream_ptr(stream)), "pars3_dot")
+    return out
 
 
 class SssDevice:

@@ -23,10 +23,21 @@ The halo here spans middle and outer entries (the reference's
 because its outer pass runs on worker 0).  The reference's
 plan arrays are not altered.
 
+Overlap: the rank's rows are split into BOUNDARY rows
+(some stored column below ``lo``: they read the x halo and emit partials)
+and INTERIOR rows (all columns in the own block).  Each part gets its own
+device plan over the same extended index space, both accumulating into one
+``y_ext`` (``pars3_plan_spmv_acc``); the interior product is enqueued right
+after the halo exchange is started, so it runs while the halo is in flight,
+and only the boundary product waits for it.  The interior plan carries the
+diagonal; the boundary plan skips rows without entries
+(``PARS3_PLAN_SKIP_EMPTY``).  With an RCM band the boundary is the first
+~bandwidth rows of the block (c5 at 8 ranks: ~9 %).
+
 Communication uses ``torch.distributed`` point-to-point ops
 (``batch_isend_irecv``): NCCL over NVLink with device tensors, or gloo with
-host staging for CPU tests.  The local product is the GPU tile kernel; tests
-may inject another local product (``local_factory``).
+host staging for CPU tests.  The local products are GPU tile kernels; tests
+may inject another local product (``local_factory``, called per part).
 """
 
 from __future__ import annotations
@@ -37,7 +48,8 @@ import numpy as np
 
 from .split import BandSplit, PartitionPlan
 
-__all__ = ["RankShard", "shard_for_rank", "exchange_schedule", "DistributedPars3"]
+__all__ = ["RankShard", "shard_for_rank", "split_shard", "exchange_schedule", "DistributedPars3",
+           "emulate_ranks"]
 
 
 @dataclass
@@ -101,6 +113,33 @@ def shard_for_rank(s: BandSplit, plan: PartitionPlan, rank: int) -> RankShard:
     return RankShard(rank, lo, hi, halo_lo, row_ptr, (col - halo_lo).astype(np.int32), val, diags)
 
 
+def split_shard(sh: RankShard):
+    """(interior, boundary) parts of a shard over the same extended space:
+    boundary rows have a stored column below ``lo`` (the halo), interior rows
+    do not.  The interior part keeps the diagonal, the boundary part has a
+    zero diagonal; ``boundary`` is None when no row reads the halo."""
+    counts = np.diff(sh.row_ptr)
+    rows = np.repeat(np.arange(sh.n_ext, dtype=np.int64), counts)
+    is_b = np.zeros(sh.n_ext, dtype=bool)
+    if sh.col_ind.size:
+        halo_rows = np.unique(rows[sh.col_ind < sh.own_off])
+        is_b[halo_rows] = True
+    if not is_b.any():
+        return sh, None
+
+    def part(keep_row, diags):
+        keep = keep_row[rows]
+        c = np.where(keep_row, counts, 0)
+        rp = np.zeros(sh.n_ext + 1, dtype=np.int64)
+        np.cumsum(c, out=rp[1:])
+        return RankShard(sh.rank, sh.lo, sh.hi, sh.halo_lo, rp, sh.col_ind[keep],
+                         sh.off_diags[keep], diags)
+
+    interior = part(~is_b, sh.diags)
+    boundary = part(is_b, np.zeros(sh.n_ext))
+    return interior, boundary
+
+
 def exchange_schedule(s: BandSplit, plan: PartitionPlan):
     """Every rank's halo range, and the (src, dst, a, b) segments: rank dst
     needs x[a, b) from owner src (and returns y partials for the same range)."""
@@ -131,13 +170,14 @@ class DistributedPars3:
     """One rank's operator: ``y_own = (A x)[lo:hi]`` from ``x_own = x[lo:hi]``.
 
     ``plan.p`` must equal the world size; rank r owns block r.  With
-    ``local_factory`` (tests) the local product is ``local_factory(shard)``
+    ``local_factory`` (tests) each local product is ``local_factory(part)``
     returning a callable ``y_ext = f(x_ext)`` on host arrays; otherwise the
-    GPU tile kernel runs it on the rank's device.
+    GPU tile kernel runs it on the rank's device.  ``overlap=False`` runs one
+    plan over all the rank's rows after the halo has arrived.
     """
 
     def __init__(self, s: BandSplit, plan: PartitionPlan, group=None, local_factory=None,
-                 device=None, options=None):
+                 device=None, options=None, overlap=True, max_ctas=0):
         import torch
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
@@ -154,19 +194,32 @@ class DistributedPars3:
         assert self.halos[self.rank] == self.shard.halo_lo
         self.staged = dist.get_backend(group) == "gloo"
         sh = self.shard
+        self.overlap = bool(overlap)
+        parts = split_shard(sh) if overlap else (sh, None)
+        self.interior_shard, self.boundary_shard = parts
         if local_factory is not None:
-            self._local = local_factory(sh)
+            self._local = [local_factory(p) if p is not None else None for p in parts]
             self.device = torch.device("cpu")
             self._on_host = True
+            self.ops = []
         else:
+            from ._lib import PLAN_SKIP_EMPTY
             from .device import Pars3Operator
             self.device = torch.device(device) if device is not None else torch.device(
                 "cuda", torch.cuda.current_device())
+            base = tuple(options or ()) + (0, 0, 0, -1, 0, 0, 0)[len(options or ()):]
             e = np.zeros(0, np.int32)
-            self._op = Pars3Operator(sh.n_ext, max(1, sh.n_ext), sh.diags, sh.row_ptr, sh.col_ind,
-                                     sh.off_diags, e, e, np.zeros(0), device=self.device,
-                                     options=options)
+
+            def make(p, flags, ctas):
+                o = base[:5] + (base[5] | flags, ctas or base[6])
+                return Pars3Operator(p.n_ext, max(1, p.n_ext), p.diags, p.row_ptr, p.col_ind,
+                                     p.off_diags, e, e, np.zeros(0), device=self.device, options=o)
+            # the interior kernel may leave SMs to the concurrent exchange
+            self.ops = [make(parts[0], 0, max_ctas)]
+            if parts[1] is not None:
+                self.ops.append(make(parts[1], PLAN_SKIP_EMPTY, 0))
             self._on_host = False
+        self._op = self.ops[0] if self.ops else None  # the dominant (interior) product
         t = torch.float64
         self.x_ext = torch.zeros(sh.n_ext, dtype=t, device=self.device)
         self.y_ext = torch.zeros(sh.n_ext, dtype=t, device=self.device)
@@ -174,12 +227,14 @@ class DistributedPars3:
                        for (src, dst, a, b) in self.segs if src == self.rank}
 
     # -- communication --------------------------------------------------
-    def _p2p(self, ops):
+    def _start(self, ops):
+        """Post point-to-point ops; returns what _finish waits on.  NCCL ops
+        run on NCCL's stream after the work already enqueued; gloo stages
+        device tensors through the host and completes here."""
         if not ops:
-            return
+            return None
         dist = self.dist
         if self.staged and not self._on_host:
-            # gloo moves host tensors: stage device buffers through the host
             host_ops, copies = [], []
             for kind, tensor, peer in ops:
                 h = tensor.detach().cpu()
@@ -192,14 +247,27 @@ class DistributedPars3:
             for tensor, h, kind in copies:
                 if kind is dist.irecv:
                     tensor.copy_(h)
-            return
-        reqs = dist.batch_isend_irecv([dist.P2POp(k, tns, peer, self.group)
+            return None
+        return dist.batch_isend_irecv([dist.P2POp(k, tns, peer, self.group)
                                        for k, tns, peer in ops])
-        for r in reqs:
+
+    @staticmethod
+    def _finish(reqs):
+        """Make the current stream wait for the posted ops (once per post)."""
+        for r in reqs or ():
             r.wait()
 
     def _peer(self, r):
         return self.dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def _local_product(self, k):
+        """Local part k (0 interior, 1 boundary) accumulated into y_ext."""
+        if self._on_host:
+            f = self._local[k]
+            if f is not None:
+                self.y_ext += self.torch.from_numpy(np.asarray(f(self.x_ext.numpy())))
+        elif k < len(self.ops):
+            self.ops[k].matvec(self.x_ext, self.y_ext, accumulate=True)
 
     def matvec(self, x_own):
         """y_own for this rank's block; x_own: length hi - lo (this rank's x)."""
@@ -207,7 +275,9 @@ class DistributedPars3:
         nown = sh.hi - sh.lo
         if x_own.shape[0] != nown:
             raise ValueError(f"x block must have {nown} entries, got {x_own.shape[0]}")
-        self.x_ext[sh.own_off:] = x_own.to(self.device)
+        if x_own.data_ptr() != self.x_ext[sh.own_off:].data_ptr():
+            self.x_ext[sh.own_off:] = x_own.to(self.device)
+        self.y_ext.zero_()
         # 1. x halo: owners send slices of their block, consumers receive
         ops = []
         for (src, dst, a, b) in self.segs:
@@ -217,12 +287,15 @@ class DistributedPars3:
                             self._peer(dst)))
             elif dst == self.rank:
                 ops.append((dist.irecv, self.x_ext[a - sh.halo_lo:b - sh.halo_lo], self._peer(src)))
-        self._p2p(ops)
-        # 2. local product over [halo_lo, hi)
-        if self._on_host:
-            self.y_ext.copy_(self.torch.from_numpy(np.asarray(self._local(self.x_ext.numpy()))))
-        else:
-            self._op.matvec(self.x_ext, self.y_ext)
+        reqs = self._start(ops)
+        # 2. interior rows while the halo is in flight, then the boundary rows
+        #    (without overlap the single product waits for the halo)
+        if not self.overlap:
+            self._finish(reqs)
+            reqs = None
+        self._local_product(0)
+        self._finish(reqs)
+        self._local_product(1)
         # 3. accumulation messages back to the owners, added in source order
         ops = []
         for (src, dst, a, b) in self.segs:
@@ -231,25 +304,42 @@ class DistributedPars3:
                             self._peer(src)))
             elif src == self.rank:
                 ops.append((dist.irecv, self._inbox[(dst, a)], self._peer(dst)))
-        self._p2p(ops)
+        self._finish(self._start(ops))
         y_own = self.y_ext[sh.own_off:].clone()
         for (src, dst, a, b) in self.segs:
             if src == self.rank:
                 y_own[a - sh.lo:b - sh.lo] += self._inbox[(dst, a)]
         return y_own
 
+    def x_view(self):
+        """This rank's block of x inside the extended buffer: writing x here
+        (e.g. the next iterate of a solver) skips matvec's copy."""
+        return self.x_ext[self.shard.own_off:]
 
-def emulate_ranks(s: BandSplit, plan: PartitionPlan, x, make_local):
+
+def emulate_ranks(s: BandSplit, plan: PartitionPlan, x, make_local, overlap=False):
     """Run the p-rank protocol sequentially in one process: the same shards,
     schedule and data movement as DistributedPars3, with the exchanges as
-    direct copies.  ``make_local(shard)`` returns ``y_ext = f(x_ext)`` (for
-    the GPU path: a tile-kernel operator on the rank's extended space).
-    Returns y as a torch tensor on ``x``'s device."""
+    direct copies.  ``make_local(shard, boundary)`` returns ``y_ext =
+    f(x_ext)`` (for the GPU path: a tile-kernel operator on the rank's
+    extended space); with ``overlap`` each rank's product is the sum of its
+    interior and boundary parts (split_shard).  Returns y as a torch tensor
+    on ``x``'s device."""
     import torch
     p = plan.p
     shards = [shard_for_rank(s, plan, w) for w in range(p)]
     halos, segs = exchange_schedule(s, plan)
-    local = [make_local(sh) for sh in shards]
+    def make(sh):
+        if not overlap:
+            return make_local(sh, False)
+        inner, bnd = split_shard(sh)
+        fi = make_local(inner, False)
+        if bnd is None:
+            return fi
+        fb = make_local(bnd, True)
+        return lambda xe: fi(xe) + fb(xe)
+
+    local = [make(sh) for sh in shards]
     x = torch.as_tensor(x, dtype=torch.float64)
     x_ext = []
     for sh in shards:

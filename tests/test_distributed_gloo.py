@@ -37,7 +37,7 @@ def _case(name):
     return m
 
 
-def _worker(rank, world, port, name, beta, out):
+def _worker(rank, world, port, name, beta, overlap, out):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -56,7 +56,7 @@ def _worker(rank, world, port, name, beta, out):
         def local(sh):
             return lambda xe: O.spmv_serial(sh.row_ptr, sh.col_ind, sh.off_diags, sh.diags, xe)
 
-        op = DistributedPars3(s, plan, local_factory=local)
+        op = DistributedPars3(s, plan, local_factory=local, overlap=overlap)
         x = np.random.default_rng(9).uniform(-1, 1, m.n)
         lo, hi = int(plan.block_start[rank]), int(plan.block_start[rank + 1])
         y_own = op.matvec(torch.from_numpy(x[lo:hi].copy()))
@@ -76,13 +76,13 @@ def _worker(rank, world, port, name, beta, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world,overlap", [(2, True), (3, True), (2, False)])
 @pytest.mark.parametrize("name,beta", [("band", 8), ("band", 4000), ("stencil", 20), ("rmat", 8)])
-def test_gloo_protocol_matches_serial(world, name, beta):
+def test_gloo_protocol_matches_serial(world, overlap, name, beta):
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, beta, out))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, beta, overlap, out))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -112,3 +112,31 @@ def test_schedule_and_shards_cover_the_matrix():
             got = sum(b - a for (src, dst, a, b) in segs if dst == w)
             assert got == need and all(src < dst for (src, dst, a, b) in segs)
         assert total == m.nnz_offdiag
+
+
+def test_split_shard_partitions_rows():
+    """Interior and boundary parts cover the shard's entries exactly once;
+    boundary rows are exactly the rows reading the halo; the diagonal stays
+    with the interior part."""
+    import paper_2407_17651_b200 as P
+    from paper_2407_17651_b200.distributed import shard_for_rank, split_shard
+    m = _case("stencil")
+    s = P.split_bands(m, 20)
+    plan, _ = P.classify_conflicts(s, P.partition_rows(m.n, 3))
+    for w in range(3):
+        sh = shard_for_rank(s, plan, w)
+        inner, bnd = split_shard(sh)
+        if w == 0:
+            assert bnd is None and inner is sh
+            continue
+        assert inner.col_ind.size + bnd.col_ind.size == sh.col_ind.size
+        assert np.array_equal(inner.diags, sh.diags) and not bnd.diags.any()
+        assert (inner.col_ind >= sh.own_off).all()
+        for r in range(sh.n_ext):
+            cols = sh.col_ind[sh.row_ptr[r]:sh.row_ptr[r + 1]]
+            b = bnd.col_ind[bnd.row_ptr[r]:bnd.row_ptr[r + 1]]
+            i = inner.col_ind[inner.row_ptr[r]:inner.row_ptr[r + 1]]
+            if cols.size and cols.min() < sh.own_off:
+                assert np.array_equal(b, cols) and i.size == 0
+            else:
+                assert np.array_equal(i, cols) and b.size == 0

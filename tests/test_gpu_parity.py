@@ -176,8 +176,9 @@ def test_spmv_dot(oracle):
     assert abs(float(dot.item()) - float(yh @ yh)) <= 1e-12 * float(yh @ yh)
 
 
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("p", [2, 3, 8])
-def test_multirank_protocol_on_one_gpu(p, oracle):
+def test_multirank_protocol_on_one_gpu(p, overlap, oracle):
     """The p-rank sharding with the GPU tile kernel as each rank's local
     product, exchanges emulated in-process (one GPU is available)."""
     import torch
@@ -189,12 +190,15 @@ def test_multirank_protocol_on_one_gpu(p, oracle):
         m, s, plan = _pipeline(g, beta=beta, p=p)
         x = G.make_x(m.n, 11)
 
-        def make_local(sh):
+        def make_local(sh, boundary):
             e = np.zeros(0, np.int32)
+            # boundary parts skip their empty rows (flags = PARS3_PLAN_SKIP_EMPTY)
             op = Pars3Operator(sh.n_ext, max(1, sh.n_ext), sh.diags, sh.row_ptr, sh.col_ind,
-                               sh.off_diags, e, e, np.zeros(0))
+                               sh.off_diags, e, e, np.zeros(0),
+                               options=(0, 0, 0, -1, 0, 1 if boundary else 0, 0))
             return lambda xe: op.matvec(xe)
 
-        y = emulate_ranks(s, plan, torch.from_numpy(x).cuda(), make_local).cpu().numpy()
+        y = emulate_ranks(s, plan, torch.from_numpy(x).cuda(), make_local,
+                          overlap=overlap).cpu().numpy()
         y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x)
         assert rel_err(y, y_ref) <= TOL, (g.name, p)
