@@ -34,6 +34,8 @@ extern "C" {
 #define PARS3_ERR_CUDA (-2)     /* maps to RuntimeError */
 #define PARS3_ERR_STRUCT (-3)   /* maps to StructuralError */
 #define PARS3_ERR_NOMEM (-4)    /* maps to MemoryError */
+#define PARS3_SLOW_PATH (-5)    /* text I/O: content outside the canonical fast-path syntax; the
+                                   caller re-reads with the exact (reference-semantics) reader */
 
 const char *pars3_last_error(void);
 int pars3_abi_version(void);
@@ -187,6 +189,38 @@ int pars3_classify_conflicts(int64_t n, const int64_t *mid_ptr, const int32_t *m
                              int64_t *row_owner, int64_t *safe_start, int64_t *conflict_idx,
                              int64_t *conflict_ptr, int64_t *conflict_target,
                              int64_t *apply_order, int64_t *apply_ptr, int64_t *halo_lo);
+
+/* ----------------------------------------------------- text file I/O */
+
+/* Matrix Market coordinate real files (replaces mmio.py:52-150 read_matrix;
+ * the expansion of symmetric/skew files and coo_normalize stay in Python).
+ * pars3_mm_open reads and checks the header and size line: *qualifier = 0
+ * general, 1 symmetric, 2 skew-symmetric.  pars3_mm_fill parses the nnz
+ * entry lines in parallel into 0-based rows/cols and values.  Both return
+ * PARS3_SLOW_PATH for any content the reference would reject or that is
+ * outside the canonical syntax (the wrapper then raises the reference's
+ * ParseError / StructuralError from its exact reader). */
+typedef struct pars3_mm_file pars3_mm_file;
+int pars3_mm_open(const char *path, pars3_mm_file **file, int64_t *n, int64_t *nnz,
+                  int32_t *qualifier);
+int pars3_mm_fill(pars3_mm_file *file, int64_t *rows, int64_t *cols, double *vals, int nthreads);
+int pars3_mm_close(pars3_mm_file *file);
+
+/* Write the selected triplets (0-based) as Matrix Market text with the
+ * given qualifier and "%.17g" values (mmio.py:152-187 after its checks). */
+int pars3_mm_write(const char *path, const char *qualifier, int64_t n, int64_t count,
+                   const int64_t *rows, const int64_t *cols, const double *vals, int nthreads);
+
+/* Dense vectors, one "%.17g" value per line (mmio.py:203-223).  Read: call
+ * with x == NULL for *count, then with x sized *count. */
+int pars3_vector_read(const char *path, double *x, int64_t *count, int nthreads);
+int pars3_vector_write(const char *path, int64_t n, const double *x, int nthreads);
+
+/* Permutation files (reorder.py:300-333): a count line then "old new" pairs.
+ * Read: call with old_idx == NULL for *n, then again; pairs in file order. */
+int pars3_permutation_read(const char *path, int64_t *n, int64_t *old_idx, int64_t *new_idx,
+                           int nthreads);
+int pars3_permutation_write(const char *path, int64_t n, const int64_t *forward, int nthreads);
 
 #ifdef __cplusplus
 }

@@ -16,10 +16,12 @@ in libpars3.so (include/pars3.h).  There is no CPU fallback for products.
 from .formats import (CooMatrix, DiagonalError, SkewReport, SkewSymmetryError, SssMatrix,
                       StructuralError, as_vector, coo_normalize, coo_to_sss, sss_to_coo,
                       validate_skew)
+from .mmio import ParseError, read_matrix, read_vector, write_matrix, write_vector
 from .mrs import MrsResult, mrs_solve
 from .parallel import prepare, spmv_atomic, spmv_pars3
 from .reorder import (AdjacencyPattern, Permutation, apply_permutation, compute_bandwidth,
-                      pattern_from_coo, pattern_from_sss, permute_sss, rcm_order)
+                      pattern_from_coo, pattern_from_sss, permute_sss, rcm_order,
+                      read_permutation, write_permutation)
 from .serial import OpCounter, count_ops, spmv_dense, spmv_serial
 from .split import (BandSplit, ConflictReport, PartitionPlan, classify_conflicts,
                     conflict_report, default_beta, merge_splits, partition_rows, split_bands)
@@ -33,5 +35,6 @@ __all__ = [
     "compute_bandwidth", "conflict_report", "coo_normalize", "coo_to_sss", "count_ops",
     "default_beta", "merge_splits", "partition_rows", "pattern_from_coo", "pattern_from_sss",
     "permute_sss", "prepare", "rcm_order", "spmv_atomic", "spmv_dense", "spmv_pars3",
-    "spmv_serial", "split_bands", "sss_to_coo", "validate_skew",
+    "spmv_serial", "split_bands", "sss_to_coo", "validate_skew", "ParseError", "read_matrix",
+    "read_vector", "write_matrix", "write_vector", "read_permutation", "write_permutation",
 ]

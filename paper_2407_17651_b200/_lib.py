@@ -21,6 +21,7 @@ PARS3_ERR_ARG = -1
 PARS3_ERR_CUDA = -2
 PARS3_ERR_STRUCT = -3
 PARS3_ERR_NOMEM = -4
+PARS3_SLOW_PATH = -5
 
 _c_i32 = ctypes.c_int32
 _c_i64 = ctypes.c_int64
@@ -76,6 +77,17 @@ _SIGS = {
                                          ctypes.POINTER(_c_i64)]),
     "pars3_split_fill": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _vp,
                                         _vp]),
+    "pars3_mm_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_vp), ctypes.POINTER(_c_i64),
+                                     ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i32)]),
+    "pars3_mm_fill": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int]),
+    "pars3_mm_close": (ctypes.c_int, [_vp]),
+    "pars3_mm_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _c_i64, _c_i64, _vp, _vp,
+                                      _vp, ctypes.c_int]),
+    "pars3_vector_read": (ctypes.c_int, [ctypes.c_char_p, _vp, ctypes.POINTER(_c_i64), ctypes.c_int]),
+    "pars3_vector_write": (ctypes.c_int, [ctypes.c_char_p, _c_i64, _vp, ctypes.c_int]),
+    "pars3_permutation_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_c_i64), _vp, _vp,
+                                              ctypes.c_int]),
+    "pars3_permutation_write": (ctypes.c_int, [ctypes.c_char_p, _c_i64, _vp, ctypes.c_int]),
     "pars3_classify_conflicts": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp,
                                                 ctypes.POINTER(_c_i64), _vp, _vp, _vp, _vp, _vp,
                                                 _vp, _vp, _vp]),

@@ -16,7 +16,8 @@ from . import _lib
 from .formats import CooMatrix, SssMatrix, StructuralError, coo_normalize
 
 __all__ = ["AdjacencyPattern", "Permutation", "pattern_from_coo", "pattern_from_sss",
-           "compute_bandwidth", "rcm_order", "apply_permutation", "permute_sss"]
+           "compute_bandwidth", "rcm_order", "apply_permutation", "permute_sss",
+           "read_permutation", "write_permutation"]
 
 
 @dataclass(frozen=True, eq=False)
@@ -147,3 +148,15 @@ def permute_sss(m: SssMatrix, perm: Permutation, nthreads: int = 0) -> SssMatrix
                                      _lib.ptr(perm.forward), _lib.ptr(rp), _lib.ptr(ci),
                                      _lib.ptr(od), _lib.ptr(dg), int(nthreads)), "permute_sss")
     return SssMatrix._trusted(m.n, rp, ci, od, dg)
+
+
+def write_permutation(path, perm: Permutation) -> None:
+    """Permutation text file (reorder.py:300-305), written natively."""
+    from .mmio import write_permutation as _w
+    _w(path, perm)
+
+
+def read_permutation(path) -> Permutation:
+    """Read a permutation file (reorder.py:308-333), parsed natively."""
+    from .mmio import read_permutation as _r
+    return _r(path)
