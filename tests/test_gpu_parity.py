@@ -132,20 +132,25 @@ def test_skew_identity_large():
 
 
 OPTION_SETS = [
-    (0, 0, 0, -1, 0),         # defaults (auto mode)
-    (0, 0, 0, -1, 1),         # ordered mode forced (owner stores + flags)
-    (0, 0, 0, -1, 2),         # accumulate mode forced
-    (64, 128, 8, 0, 1),       # tiny tiles: splits, list-mode tiles, hub chunks; ordered
+    # (tile_rows, local_slots, seg_max, gap, mode[, flags, max_ctas])
+    (0, 0, 0, -1, 0),         # defaults (auto accumulation)
+    (0, 0, 0, -1, 1),         # three-word fixed point forced
+    (0, 0, 0, -1, 2),         # fp64 shared accumulators forced
+    (0, 0, 0, -1, 3),         # two-word fixed point forced (refused for hub-heavy plans)
+    (64, 128, 8, 0, 1),       # tiny tiles: splits, list-mode tiles, hub chunks
     (64, 128, 8, 0, 2),
+    (64, 128, 8, 0, 3),
     (32, 64, 4, 2, 1),        # smallest local space: every wide row is chunked
     (4096, 65535, 64, 64, 1),   # clamped to the shared-memory budget
+    (0, 0, 0, -1, 0, 0, 37),  # persistent grid capped at 37 CTAs
 ]
 
 
 @pytest.mark.parametrize("opts", OPTION_SETS)
 def test_tile_plan_options(opts, oracle):
     """The windowed tile plan under extreme options (tile splits, hub-row
-    chunking into helper tiles, many tiny windows) against the oracle."""
+    chunking into helper tiles, many tiny windows, every accumulation mode)
+    against the oracle."""
     from paper_2407_17651_b200 import generators as G
     from paper_2407_17651_b200.device import operator_for_sss
     import torch
@@ -156,12 +161,44 @@ def test_tile_plan_options(opts, oracle):
         m = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
         x = G.make_x(m.n, 9)
         y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x)
-        op = operator_for_sss(m, options=opts)
+        try:
+            op = operator_for_sss(m, options=opts)
+        except ValueError as e:  # two words cannot hold a hub column's terms
+            assert opts[4] == 3 and "two-word" in str(e), (g.name, opts, e)
+            continue
         y = op.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
         assert rel_err(y, y_ref) <= TOL, (g.name, opts, op.stats())
-        for _ in range(3):  # repeated launches reuse the plan (epoch flags)
+        for _ in range(3):  # repeated launches reuse the plan
             y2 = op.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
             assert rel_err(y2, y_ref) <= TOL
+
+
+def test_accumulating_plans_and_skip_empty(oracle):
+    """Two partial plans (rows split by parity) accumulate into one y
+    (pars3_plan_spmv_acc); the diagonal lives in the first, the second skips
+    its empty rows (PARS3_PLAN_SKIP_EMPTY)."""
+    import torch
+    from paper_2407_17651_b200 import generators as G
+    from paper_2407_17651_b200.device import Pars3Operator
+    g = G.stencil27(16, seed_val=2, alpha=0.5)
+    m = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
+    rows = np.repeat(np.arange(m.n), np.diff(m.row_ptr))
+    x = G.make_x(m.n, 3)
+    y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x)
+    e = np.zeros(0, np.int32)
+    ops = []
+    for parity, diag, flags in ((0, m.diags, 0), (1, np.zeros(m.n), 1)):
+        keep_row = (np.arange(m.n) % 2) == parity
+        keep = keep_row[rows]
+        rp = np.zeros(m.n + 1, dtype=np.int64)
+        np.cumsum(np.where(keep_row, np.diff(m.row_ptr), 0), out=rp[1:])
+        ops.append(Pars3Operator(m.n, m.n, diag, rp, m.col_ind[keep], m.off_diags[keep], e, e,
+                                 np.zeros(0), options=(0, 0, 0, -1, 0, flags, 0)))
+    xd = torch.from_numpy(x).cuda()
+    y = torch.full((m.n,), 7.0, dtype=torch.float64, device="cuda")
+    ops[0].matvec(xd, y)                     # overwrites y
+    ops[1].matvec(xd, y, accumulate=True)    # adds
+    assert rel_err(y.cpu().numpy(), y_ref) <= TOL
 
 
 def test_spmv_dot(oracle):
