@@ -75,7 +75,13 @@ def build_problem(cfg: str, beta=None):
     t1 = time.time()
     m0 = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
     del g
-    perm = P.rcm_order(P.pattern_from_sss(m0))
+    try:
+        import torch
+        gpu = torch.cuda.is_available()
+    except Exception:
+        gpu = False
+    # GPU RCM (same labels as the reference, tests/test_gpu_rcm.py) when a device is present
+    perm = P.rcm_order_sss(m0) if gpu else P.rcm_order(P.pattern_from_sss(m0))
     t2 = time.time()
     m = P.permute_sss(m0, perm)
     del m0
@@ -86,7 +92,8 @@ def build_problem(cfg: str, beta=None):
     t3 = time.time()
     x = G.make_x(m.n, G.CONFIGS[cfg]["seed_x"])
     log(f"{cfg}: n={m.n} m={m.nnz_offdiag} rcm_bw={bw} beta={beta} mid={s.middle_count} "
-        f"outer={s.outer_count}; gen {t1 - t0:.1f}s rcm {t2 - t1:.1f}s permute+split {t3 - t2:.1f}s")
+        f"outer={s.outer_count}; gen {t1 - t0:.1f}s rcm ({'gpu' if gpu else 'host'}) {t2 - t1:.2f}s "
+        f"permute+split {t3 - t2:.1f}s")
     return m, s, bw, beta, np.ascontiguousarray(x)
 
 

@@ -162,6 +162,20 @@ int pars3_pattern_from_lower(int64_t n, const int64_t *row_ptr, const int32_t *c
 int pars3_rcm_order(int64_t n, const int64_t *indptr, const int32_t *indices, int64_t *forward,
                     int nthreads);
 
+/* rcm_order on the GPU (device arrays, `stream`): the same labels as
+ * pars3_rcm_order and the reference (reorder.py:137-286), all components
+ * processed in lockstep by level-synchronous multi-source BFS with CUB radix
+ * sorts per level (csrc/rcm.cu).  Neighbour lists may be in any order.
+ * Synchronises `stream` (level sizes steer the host loop). */
+int pars3_rcm_order_device(int64_t n, const int64_t *indptr, const int32_t *indices,
+                           int64_t *forward, void *stream);
+
+/* The same from a strictly-lower SSS pattern on the device (row_ptr[n+1],
+ * col_ind[nnz]): the symmetric adjacency is built on the device first
+ * (replaces pattern_from_coo + rcm_order). */
+int pars3_rcm_order_lower_device(int64_t n, const int64_t *row_ptr, const int32_t *col_ind,
+                                 int64_t nnz, int64_t *forward, void *stream);
+
 /* Relabel an SSS matrix: replaces coo_to_sss(apply_permutation(coo, perm))
  * (reorder.py:289-297, formats.py:413-475) without the COO round trip.
  * Output arrays sized like the input. */

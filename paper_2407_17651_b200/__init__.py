@@ -20,7 +20,7 @@ from .mmio import ParseError, read_matrix, read_vector, write_matrix, write_vect
 from .mrs import MrsResult, mrs_solve
 from .parallel import prepare, spmv_atomic, spmv_pars3
 from .reorder import (AdjacencyPattern, Permutation, apply_permutation, compute_bandwidth,
-                      pattern_from_coo, pattern_from_sss, permute_sss, rcm_order,
+                      pattern_from_coo, pattern_from_sss, permute_sss, rcm_order, rcm_order_sss,
                       read_permutation, write_permutation)
 from .serial import OpCounter, count_ops, spmv_dense, spmv_serial
 from .split import (BandSplit, ConflictReport, PartitionPlan, classify_conflicts,
@@ -36,5 +36,5 @@ __all__ = [
     "default_beta", "merge_splits", "partition_rows", "pattern_from_coo", "pattern_from_sss",
     "permute_sss", "prepare", "rcm_order", "spmv_atomic", "spmv_dense", "spmv_pars3",
     "spmv_serial", "split_bands", "sss_to_coo", "validate_skew", "ParseError", "read_matrix",
-    "read_vector", "write_matrix", "write_vector", "read_permutation", "write_permutation",
+    "read_vector", "write_matrix", "write_vector", "read_permutation", "write_permutation", "rcm_order_sss",
 ]

@@ -71,6 +71,8 @@ _SIGS = {
                                         ctypes.c_double, _vp, _vp]),
     "pars3_pattern_from_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
     "pars3_rcm_order": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, ctypes.c_int]),
+    "pars3_rcm_order_device": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
+    "pars3_rcm_order_lower_device": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp]),
     "pars3_permute_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                            ctypes.c_int]),
     "pars3_split_count": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, ctypes.POINTER(_c_i64),

@@ -17,7 +17,7 @@ from .formats import CooMatrix, SssMatrix, StructuralError, coo_normalize
 
 __all__ = ["AdjacencyPattern", "Permutation", "pattern_from_coo", "pattern_from_sss",
            "compute_bandwidth", "rcm_order", "apply_permutation", "permute_sss",
-           "read_permutation", "write_permutation"]
+           "read_permutation", "write_permutation", "rcm_order_sss"]
 
 
 @dataclass(frozen=True, eq=False)
@@ -116,13 +116,54 @@ def compute_bandwidth(m) -> int:
     raise TypeError(f"expected CooMatrix or SssMatrix, got {type(m).__name__}")
 
 
-def rcm_order(pattern: AdjacencyPattern, nthreads: int = 0) -> Permutation:
-    """Reverse Cuthill-McKee labels, bit-identical to reorder.py:251-286."""
+def _upload(a, dtype, dev):
+    """Host array -> device tensor (frozen arrays are read, never written)."""
+    import warnings
+
+    import torch
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)  # torch warns on read-only numpy buffers
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(dev)
+
+
+def rcm_order(pattern: AdjacencyPattern, nthreads: int = 0, device=None) -> Permutation:
+    """Reverse Cuthill-McKee labels, bit-identical to reorder.py:251-286.
+
+    Host-native by default (``nthreads`` OpenMP threads); with ``device``
+    (e.g. ``"cuda"``) the pattern is uploaded and ordered on the GPU
+    (``pars3_rcm_order_device``), same labels."""
     L = _lib.load()
+    if device is not None:
+        from .device import require_cuda
+        torch = require_cuda()
+        dev = torch.device(device)
+        ip = _upload(pattern.indptr, np.int64, dev)
+        ix = _upload(pattern.indices, np.int32, dev)
+        fw = torch.empty(pattern.n, dtype=torch.int64, device=dev)
+        with torch.cuda.device(dev):
+            _lib.check(L.pars3_rcm_order_device(pattern.n, _lib.ptr(ip), _lib.ptr(ix), _lib.ptr(fw),
+                                                _lib.stream_ptr()), "rcm_order")
+        return Permutation(fw.cpu().numpy())
     fw = np.empty(pattern.n, dtype=np.int64)
     _lib.check(L.pars3_rcm_order(pattern.n, _lib.ptr(pattern.indptr), _lib.ptr(pattern.indices),
                                  _lib.ptr(fw), int(nthreads)), "rcm_order")
     return Permutation(fw)
+
+
+def rcm_order_sss(m: SssMatrix, device="cuda") -> Permutation:
+    """``rcm_order(pattern_from_sss(m))`` on the GPU: the symmetric adjacency is
+    built on the device from the skyline arrays, then ordered there."""
+    from .device import require_cuda
+    torch = require_cuda()
+    dev = torch.device(device)
+    rp = _upload(m.row_ptr, np.int64, dev)
+    ci = _upload(m.col_ind, np.int32, dev)
+    fw = torch.empty(m.n, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().pars3_rcm_order_lower_device(
+            m.n, _lib.ptr(rp), _lib.ptr(ci), int(m.nnz_offdiag), _lib.ptr(fw), _lib.stream_ptr()),
+            "rcm_order_sss")
+    return Permutation(fw.cpu().numpy())
 
 
 def apply_permutation(m: CooMatrix, perm: Permutation) -> CooMatrix:

@@ -1,0 +1,74 @@
+"""GPU reverse Cuthill-McKee (csrc/rcm.cu) against the host-native RCM,
+which is pinned bit-exactly to the reference (test_prep_parity.py,
+test_config_hashes.py), and against the reference's own labels for the
+BASELINE configs c2-c4 (tests/golden/hashes.json)."""
+
+import numpy as np
+import pytest
+
+import paper_2407_17651_b200 as P
+from conftest import sha
+
+pytestmark = pytest.mark.gpu
+
+
+def _sss(g):
+    return P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
+
+
+def _lower_from_pairs(n, pairs):
+    """Strictly-lower SSS of an undirected edge set (values 1)."""
+    pairs = {(max(a, b), min(a, b)) for a, b in pairs if a != b}
+    rows = np.array(sorted(pairs), dtype=np.int64).reshape(-1, 2)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rp, rows[:, 0] + 1, 1)
+    np.cumsum(rp, out=rp)
+    return P.SssMatrix(n, rp, rows[:, 1], np.ones(len(rows)), np.zeros(n))
+
+
+def _graphs():
+    from paper_2407_17651_b200 import generators as G
+    rng = np.random.default_rng(5)
+    yield "rmat12", _sss(G.rmat(12, 16, seed_struct=3, seed_perm=4, seed_val=5))
+    yield "rmat14_ef4", _sss(G.rmat(14, 4, seed_struct=6, seed_perm=7, seed_val=8))
+    yield "band", _sss(G.random_band(20000, 300, 8, 0.01, seed_struct=1, seed_perm=2, seed_val=3))
+    yield "stencil27", _sss(G.stencil27(20, seed_perm=9, seed_val=6))
+    yield "grid5", _sss(G.grid5(60, seed_perm=7, seed_val=8))
+    # many small components of different shapes, isolated nodes between them
+    pairs, base = [], 0
+    for k in range(300):
+        size = int(rng.integers(1, 9))
+        kind = k % 3
+        nodes = base + rng.permutation(size)
+        if kind == 0:
+            pairs += [(nodes[i], nodes[i + 1]) for i in range(size - 1)]          # path
+        elif kind == 1:
+            pairs += [(nodes[0], nodes[i]) for i in range(1, size)]              # star
+        else:
+            pairs += [(nodes[i], nodes[j]) for i in range(size) for j in range(i)]  # clique
+        base += size + int(rng.integers(0, 3))
+    perm = rng.permutation(base)
+    yield "small_components", _lower_from_pairs(base, [(perm[a], perm[b]) for a, b in pairs])
+    yield "all_isolated", P.SssMatrix(7, np.zeros(8, np.int64), [], [], np.zeros(7))
+    yield "single", P.SssMatrix(1, np.zeros(2, np.int64), [], [], np.zeros(1))
+    yield "two_paths_reversed", _lower_from_pairs(10, [(9, 8), (8, 7), (0, 5), (5, 3), (3, 1)])
+
+
+@pytest.mark.parametrize("name,m", list(_graphs()), ids=lambda v: v if isinstance(v, str) else "")
+def test_gpu_rcm_equals_native(name, m, lib_built):
+    pat = P.pattern_from_sss(m)
+    want = P.rcm_order(pat).forward
+    assert np.array_equal(P.rcm_order(pat, device="cuda").forward, want), name
+    assert np.array_equal(P.rcm_order_sss(m).forward, want), name
+
+
+def test_gpu_rcm_empty(lib_built):
+    m = P.SssMatrix(0, np.zeros(1, np.int64), [], [], np.zeros(0))
+    assert P.rcm_order_sss(m).n == 0
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_gpu_rcm_reference_labels(cfg, golden_hashes, lib_built):
+    from paper_2407_17651_b200 import generators as G
+    g = G.make_config(cfg)
+    assert sha(P.rcm_order_sss(_sss(g)).forward) == golden_hashes[cfg]["rcm_forward"]
