@@ -95,6 +95,65 @@ class Pars3Operator:
                                                _lib.stream_ptr(stream)), "pars3_plan_spmv_dot")
         return y, dot
 
+    # -- host-resident vectors: pipelined copies --------------------------
+    def matvec_host(self, x, out=None, non_blocking=False):
+        """y = A x for a HOST float64 tensor x (pinned for overlap), result in
+        the host tensor ``out``.  Three streams and double-buffered device
+        vectors pipeline consecutive calls: call k+1's host->device copy runs
+        on the copy engine while call k's product and device->host copy are
+        still in flight (PCIe is full duplex).  With ``non_blocking`` the call
+        returns once the work is enqueued: ``out`` (and re-use of ``x``) is
+        safe after ``torch.cuda.synchronize()`` or ``self.host_sync()``."""
+        torch = self.torch
+        pl = getattr(self, "_pipe", None)
+        if pl is None:
+            dev = self.device
+            pl = self._pipe = {
+                "k": 0,
+                "h2d": torch.cuda.Stream(dev), "comp": torch.cuda.Stream(dev),
+                "d2h": torch.cuda.Stream(dev),
+                "x": [torch.empty(self.n, dtype=torch.float64, device=dev) for _ in range(2)],
+                "y": [torch.empty(self.n, dtype=torch.float64, device=dev) for _ in range(2)],
+                "ev_x": [torch.cuda.Event() for _ in range(2)],
+                "ev_y": [torch.cuda.Event() for _ in range(2)],
+                "ev_out": [torch.cuda.Event() for _ in range(2)],
+            }
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.float64, pin_memory=x.is_pinned())
+        b = pl["k"] & 1
+        pl["k"] += 1
+        h2d, comp, d2h = pl["h2d"], pl["comp"], pl["d2h"]
+        # buffer b is free once call k-2's product (reads x[b]) and copy-out
+        # (reads y[b]) are done
+        h2d.wait_event(pl["ev_y"][b])
+        with torch.cuda.stream(h2d):
+            pl["x"][b].copy_(x, non_blocking=True)
+        pl["ev_x"][b].record(h2d)
+        comp.wait_event(pl["ev_x"][b])
+        comp.wait_event(pl["ev_out"][b])
+        self.matvec(pl["x"][b], pl["y"][b], stream=comp)
+        pl["ev_y"][b].record(comp)
+        d2h.wait_event(pl["ev_y"][b])
+        with torch.cuda.stream(d2h):
+            out.copy_(pl["y"][b], non_blocking=True)
+        pl["ev_out"][b].record(d2h)
+        if not non_blocking:
+            pl["ev_out"][b].synchronize()
+        return out
+
+    def host_join(self, stream=None):
+        """Make ``stream`` (default: the current stream) wait for every
+        pipelined host product, without blocking the host."""
+        pl = getattr(self, "_pipe", None)
+        if pl is not None:
+            (stream or self.torch.cuda.current_stream(self.device)).wait_stream(pl["d2h"])
+
+    def host_sync(self):
+        """Wait for every pipelined host product (matvec_host)."""
+        pl = getattr(self, "_pipe", None)
+        if pl is not None:
+            pl["d2h"].synchronize()
+
     def kernel_count(self, with_dot: bool = False) -> int:
         c = ctypes.c_int32()
         _lib.check(self._L.pars3_plan_kernel_count(self._handle, int(with_dot), ctypes.byref(c)))

@@ -40,14 +40,17 @@ def prepare(s: BandSplit, plan: PartitionPlan | None = None, device=None):
     return operator_for_split(s, p=p, block_start=bs, device=device)
 
 
-def spmv_pars3(s: BandSplit, plan: PartitionPlan, x, p: int | None = None, out=None):
+def spmv_pars3(s: BandSplit, plan: PartitionPlan, x, p: int | None = None, out=None,
+               non_blocking=False):
     """Staged 3-way product y = A x (GPU).  numpy in -> numpy out; CUDA
-    tensor in -> CUDA tensor out (optionally into ``out``)."""
+    tensor in -> CUDA tensor out (optionally into ``out``); pinned host
+    tensor in -> host tensor out, with ``non_blocking`` pipelining the copies
+    of consecutive calls (result ready after torch.cuda.synchronize())."""
     _check_pair(s, plan, p)
     if not hasattr(x, "data_ptr"):
         x = as_vector(x, s.n)
     from .serial import _run
-    return _run(prepare(s, plan), x, s.n, out)
+    return _run(prepare(s, plan), x, s.n, out, non_blocking)
 
 
 def spmv_atomic(m: SssMatrix, x, t: int = 1, out=None):

@@ -34,9 +34,11 @@ def count_ops(m: SssMatrix) -> OpCounter:
     return OpCounter(element_reads=m.nnz_offdiag + m.n, multiply_adds=2 * m.nnz_offdiag + m.n)
 
 
-def _run(op, x, n, out=None):
+def _run(op, x, n, out=None, non_blocking=False):
     """Dispatch on the input's home: CUDA tensor -> CUDA result; host torch
-    tensor (pinned for async copies) -> host tensor (into ``out`` if given);
+    tensor (pinned for async copies) -> host tensor (into ``out`` if given),
+    through the operator's copy pipeline (``non_blocking``: consecutive calls
+    overlap their copies; the result is ready after torch.cuda.synchronize());
     anything else -> numpy."""
     from .device import require_cuda
     torch = require_cuda()
@@ -44,13 +46,9 @@ def _run(op, x, n, out=None):
         if x.dim() != 1 or x.shape[0] != n:
             raise ValueError(f"x must be a vector of length {n}, got shape {tuple(x.shape)}")
         if not x.is_cuda:
-            xd = x.to(device=op.device, dtype=torch.float64, non_blocking=True)
-            yd = op.matvec(xd)
-            if out is None:
-                out = torch.empty(n, dtype=torch.float64, pin_memory=x.is_pinned())
-            out.copy_(yd, non_blocking=True)
-            torch.cuda.current_stream(op.device).synchronize()
-            return out
+            if x.dtype != torch.float64:
+                x = x.to(torch.float64)
+            return op.matvec_host(x.contiguous(), out, non_blocking=non_blocking)
         xd = x.to(device=op.device, dtype=torch.float64).contiguous()
         return op.matvec(xd, out)
     xv = as_vector(x, n)
@@ -60,13 +58,13 @@ def _run(op, x, n, out=None):
     return op.matvec(xd).cpu().numpy()
 
 
-def spmv_serial(m: SssMatrix, x, out=None):
-    """y = A x for a skyline matrix (GPU).  numpy in -> numpy out; a torch
-    tensor in -> a CUDA tensor out."""
+def spmv_serial(m: SssMatrix, x, out=None, non_blocking=False):
+    """y = A x for a skyline matrix (GPU).  numpy in -> numpy out; a CUDA
+    tensor in -> a CUDA tensor out; a host tensor in -> a host tensor out."""
     from .device import operator_for_sss
     if not hasattr(x, "data_ptr"):
         as_vector(x, m.n)
-    return _run(operator_for_sss(m), x, m.n, out)
+    return _run(operator_for_sss(m), x, m.n, out, non_blocking)
 
 
 def spmv_dense(m, x) -> np.ndarray:

@@ -239,3 +239,23 @@ def test_multirank_protocol_on_one_gpu(p, overlap, oracle):
                           overlap=overlap).cpu().numpy()
         y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x)
         assert rel_err(y, y_ref) <= TOL, (g.name, p)
+
+
+def test_host_pipeline_non_blocking(oracle):
+    """Pinned host vectors through spmv_pars3(non_blocking=True): five calls
+    in flight on the copy pipeline (double-buffered device vectors), each
+    result checked after one synchronize; then a blocking call."""
+    import torch
+    from paper_2407_17651_b200 import generators as G
+    g = G.stencil27(24, seed_val=5, alpha=0.5)
+    m, s, plan = _pipeline(g)
+    xs = [torch.from_numpy(G.make_x(m.n, 20 + k)).pin_memory() for k in range(5)]
+    outs = [torch.empty(m.n, dtype=torch.float64).pin_memory() for _ in range(5)]
+    for x, o in zip(xs, outs):
+        P.spmv_pars3(s, plan, x, out=o, non_blocking=True)
+    torch.cuda.synchronize()
+    for x, o in zip(xs, outs):
+        y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x.numpy())
+        assert rel_err(o.numpy(), y_ref) <= TOL
+    y = P.spmv_pars3(s, plan, xs[0])  # blocking; y's cross-tile reductions are unordered
+    assert not y.is_cuda and rel_err(y.numpy(), outs[0].numpy()) <= TOL
