@@ -13,9 +13,12 @@ Drop-in for the hot path of the reference package ``skewspmv``
 in libpars3.so (include/pars3.h).  There is no CPU fallback for products.
 """
 
-from .formats import (CooMatrix, DiagonalError, SkewReport, SkewSymmetryError, SssMatrix,
-                      StructuralError, as_vector, coo_normalize, coo_to_sss, sss_to_coo,
-                      validate_skew)
+from .formats import (CooMatrix, CsrMatrix, DiagonalError, SkewReport, SkewSymmetryError,
+                      SssMatrix, StructuralError, as_vector, coo_normalize, coo_to_csr, coo_to_sss,
+                      sss_to_coo, validate_skew)
+from .generate import generate_band_skew
+from .instrument import (AccumulationMessage, Pars3Trace, WorkerContext, spmv_pars3_instrumented,
+                         spmv_serial_instrumented)
 from .mmio import ParseError, read_matrix, read_vector, write_matrix, write_vector
 from .mrs import MrsResult, mrs_solve
 from .parallel import prepare, spmv_atomic, spmv_pars3
@@ -36,5 +39,7 @@ __all__ = [
     "default_beta", "merge_splits", "partition_rows", "pattern_from_coo", "pattern_from_sss",
     "permute_sss", "prepare", "rcm_order", "spmv_atomic", "spmv_dense", "spmv_pars3",
     "spmv_serial", "split_bands", "sss_to_coo", "validate_skew", "ParseError", "read_matrix",
-    "read_vector", "write_matrix", "write_vector", "read_permutation", "write_permutation", "rcm_order_sss",
+    "read_vector", "write_matrix", "write_vector", "read_permutation", "write_permutation", "rcm_order_sss", "CsrMatrix", "coo_to_csr",
+    "generate_band_skew", "AccumulationMessage", "Pars3Trace", "WorkerContext",
+    "spmv_pars3_instrumented", "spmv_serial_instrumented",
 ]
