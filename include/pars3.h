@@ -87,6 +87,7 @@ typedef struct pars3_plan_options {
 } pars3_plan_options;
 
 #define PARS3_PLAN_SKIP_EMPTY 1
+#define PARS3_PLAN_CUT_BLOCKS 4  /* no window straddles block_start[1..p-1] (peer mode) */
 
 /* Build the device plan of a split on the current device: replaces the
  * per-call setup of _pars3 (parallel.py:136-183).  The split's diagonal,
@@ -97,6 +98,31 @@ typedef struct pars3_plan_options {
  * a single-GPU plan passes p = 1. */
 int pars3_plan_create(const pars3_split_view *split, const pars3_plan_options *options,
                       int32_t p, const int64_t *block_start, pars3_plan **out, void *stream);
+
+/* Peer mode (multi-GPU, one process per GPU): the plan covers rank `me`'s
+ * extended range [col_base, col_base + n) of global columns (built with
+ * PARS3_PLAN_CUT_BLOCKS and the same block_start).  x_ptrs[r] is rank r's x
+ * block and inbox_ptrs[r] its inbox (rank r's rows, zeroed by r), both as
+ * device pointers valid on this device (peer-mapped over NVLink, e.g. from
+ * pars3_ipc_open).  The kernel then reads other ranks' x and reduces the
+ * mirror sums of their rows into their inboxes directly: the halo exchange
+ * and the accumulation messages of the reference's protocol
+ * (parallel.py:96-113) run inside the product.  The caller's
+ * x / y passed to pars3_plan_spmv are addressed by local index (own block at
+ * local index block_start[me] - col_base).  nranks = 0 turns it off. */
+int pars3_plan_set_peers(pars3_plan *plan, int32_t nranks, int32_t me, int64_t col_base,
+                         const int64_t *block_start, const uint64_t *x_ptrs,
+                         const uint64_t *inbox_ptrs);
+
+/* Device memory shareable across processes (CUDA IPC) for peer mode:
+ * allocate, export a 64-byte handle, open a peer's handle (mapped into this
+ * device's address space; P2P access over NVLink when on another GPU),
+ * close / free. */
+int pars3_ipc_alloc(int64_t bytes, void **ptr);
+int pars3_ipc_free(void *ptr);
+int pars3_ipc_handle(void *ptr, uint8_t *handle64);
+int pars3_ipc_open(const uint8_t *handle64, void **ptr);
+int pars3_ipc_close(void *ptr);
 
 /* y = A x through a plan: replaces _pars3 (parallel.py:60-120, wrapper
  * spmv_pars3 parallel.py:136-183).  y is overwritten. */

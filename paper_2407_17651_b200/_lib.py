@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libpars3.so")
+# PARS3_LIB overrides the library path (A/B builds of the same ABI)
+LIB_PATH = os.environ.get("PARS3_LIB") or os.path.join(_HERE, "_build", "libpars3.so")
 
 PARS3_OK = 0
 PARS3_ERR_ARG = -1
@@ -46,6 +47,7 @@ class PlanOptions(ctypes.Structure):
 
 
 PLAN_SKIP_EMPTY = 1
+PLAN_CUT_BLOCKS = 4
 
 
 # name -> (restype, argtypes)
@@ -57,6 +59,12 @@ _SIGS = {
                                          _c_i32, _vp, ctypes.POINTER(_vp), _vp]),
     "pars3_plan_spmv": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "pars3_plan_spmv_acc": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "pars3_plan_set_peers": (ctypes.c_int, [_vp, _c_i32, _c_i32, _c_i64, _vp, _vp, _vp]),
+    "pars3_ipc_alloc": (ctypes.c_int, [_c_i64, ctypes.POINTER(_vp)]),
+    "pars3_ipc_free": (ctypes.c_int, [_vp]),
+    "pars3_ipc_handle": (ctypes.c_int, [_vp, _vp]),
+    "pars3_ipc_open": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
+    "pars3_ipc_close": (ctypes.c_int, [_vp]),
     "pars3_plan_spmv_dot": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_plan_bytes": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i64)]),
     "pars3_dot": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),

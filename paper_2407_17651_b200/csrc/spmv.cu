@@ -80,3 +80,37 @@ extern "C" int pars3_sss_spmv_atomic(int32_t n, const int32_t *row_ptr, const in
     return PARS3_OK;
 }
 
+
+// ---- CUDA IPC buffers for the peer-mode multi-GPU product -----------------
+extern "C" int pars3_ipc_alloc(int64_t bytes, void **ptr) {
+    if (!ptr || bytes < 0) PARS3_FAIL(PARS3_ERR_ARG, "bad argument");
+    CUDA_TRY(cudaMalloc(ptr, bytes > 0 ? (size_t)bytes : 16));
+    return PARS3_OK;
+}
+
+extern "C" int pars3_ipc_free(void *ptr) {
+    if (ptr) CUDA_TRY(cudaFree(ptr));
+    return PARS3_OK;
+}
+
+extern "C" int pars3_ipc_handle(void *ptr, uint8_t *handle64) {
+    if (!ptr || !handle64) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    CUDA_TRY(cudaIpcGetMemHandle(&h, ptr));
+    memcpy(handle64, &h, 64);
+    return PARS3_OK;
+}
+
+extern "C" int pars3_ipc_open(const uint8_t *handle64, void **ptr) {
+    if (!ptr || !handle64) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return PARS3_OK;
+}
+
+extern "C" int pars3_ipc_close(void *ptr) {
+    if (ptr) CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+    return PARS3_OK;
+}

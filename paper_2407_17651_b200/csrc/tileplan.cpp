@@ -87,6 +87,27 @@ void make_windows(std::vector<int32_t> &cols, int32_t gap, bool align, int64_t n
     }
 }
 
+// split windows at the cut points (rank boundaries in peer mode): a window
+// then reads x from, and delivers to, one owner
+void cut_windows(const std::vector<int32_t> &cuts, Draft &d) {
+    if (cuts.empty()) return;
+    std::vector<int32_t> lo2, len2;
+    for (size_t w = 0; w < d.wlo.size(); w++) {
+        int32_t lo = d.wlo[w];
+        const int32_t hi = lo + d.wlen[w];
+        auto it = std::upper_bound(cuts.begin(), cuts.end(), lo);
+        for (; it != cuts.end() && *it < hi; ++it) {
+            lo2.push_back(lo);
+            len2.push_back(*it - lo);
+            lo = *it;
+        }
+        lo2.push_back(lo);
+        len2.push_back(hi - lo);
+    }
+    d.wlo.swap(lo2);
+    d.wlen.swap(len2);
+}
+
 void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
                  std::vector<Draft> &out, std::vector<int32_t> &scratch) {
     scratch.clear();
@@ -110,6 +131,7 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
     d.r0 = a;
     d.r1 = b;
     make_windows(scratch, o.gap, true, R.n, d);
+    cut_windows(o.cuts, d);
     // too fragmented for windows: the tile will carry an explicit column
     // list, so do not pay for gap or alignment slots
     if ((int)d.wlo.size() > kMaxWindows) make_windows(scratch, 0, false, R.n, d);

@@ -30,6 +30,7 @@ struct PlanOptions {
                                 // 3 fixed point (2 words) (tiles.cu)
     uint16_t sink = kNoSlot;    // local slot that padding lanes / entries point at (> local_slots)
     bool skip_empty = false;    // rows without entries get no own slot (no diagonal term)
+    std::vector<int32_t> cuts;  // ascending local indices no window may straddle (peer mode)
 };
 
 constexpr int kMaxWindows = 8;  // more windows than this -> explicit column list

@@ -62,6 +62,29 @@ struct Layout {
     static constexpr int kSmem = kStride * (kWords == 3 ? 20 : 16);
 };
 
+// Peer mode (DistributedPars3(mode="peer")): the plan's index space is a
+// rank's extended range [col_base, hi); columns below its own block belong
+// to earlier ranks.  Their x is read straight from the owner's buffer and
+// their mirror sums are reduced straight into the owner's inbox, both
+// through peer-mapped (NVLink) device pointers: the halo exchange and the
+// accumulation messages happen inside the kernel.  Windows never straddle
+// a block boundary (the plan cuts them there).
+constexpr int kMaxRanks = 8;
+struct Peers {
+    int32_t nranks;   // 0: single-GPU plan
+    int32_t me;
+    int64_t col_base;                    // global column of local index 0
+    int64_t bs[kMaxRanks + 1];           // block_start (global rows)
+    const double *x[kMaxRanks];          // rank r's x block (x[r][g - bs[r]])
+    double *y[kMaxRanks];                // rank r's inbox (me: unused, own y is the kernel's y)
+};
+
+__device__ __forceinline__ int owner_of(const Peers &pr, int64_t g) {
+    int r = 0;
+    while (r + 1 < pr.nranks && g >= pr.bs[r + 1]) r++;
+    return r;
+}
+
 struct DevPlan {
     const TileMeta *tiles;
     const Window *wins;
@@ -79,6 +102,7 @@ struct DevPlan {
                  // fetched, bit 1 each warp's slice pf_dist iterations ahead, bit 2 the
                  // next tile's first slices at the end of the stream
     int32_t pf_dist;
+    Peers peers;  // multi-GPU peer mode (nranks > 0): columns owned by other ranks
 };
 
 __device__ __forceinline__ uint32_t saddr(const void *p) {
@@ -148,8 +172,10 @@ struct TileCache {
     TileMeta m;
     int32_t nw;  // windows (window mode), 0 for list mode / past the end
     int32_t lo[kMaxWindowsDev], len[kMaxWindowsDev], off[kMaxWindowsDev];
+    int32_t own[kMaxWindowsDev];  // peer mode: owning rank of each window (else me)
 };
 
+template <bool kPeer>
 __device__ __forceinline__ void fetch_tile(const DevPlan &P, int32_t t, TileCache &tc) {
     tc.nw = 0;
     if (t >= P.ntiles) {
@@ -169,21 +195,34 @@ __device__ __forceinline__ void fetch_tile(const DevPlan &P, int32_t t, TileCach
         tc.lo[w] = __ldg(&P.wins[m.w0 + w].lo);
         tc.len[w] = __ldg(&P.wins[m.w0 + w].len);
         tc.off[w] = __ldg(&P.wins[m.w0 + w].loff);
+        if (kPeer) tc.own[w] = owner_of(P.peers, P.peers.col_base + tc.lo[w]);
     }
+}
+
+// a window is moved by TMA when it is 16-byte aligned and local (peer
+// windows are gathered with plain loads over NVLink)
+template <bool kPeer>
+__device__ __forceinline__ bool tma_ok(const Peers &pr, const double *x, const TileCache &tc, int w) {
+    if (!kPeer) return tma_window(tc.lo[w], tc.len[w]);  // x is 16-byte aligned, offsets even
+    // source, size and shared destination (xs is 128-byte aligned) all 16-byte aligned
+    return ((reinterpret_cast<uintptr_t>(x + tc.lo[w]) | (uintptr_t)tc.len[w] * 8 |
+             (uintptr_t)tc.off[w] * 8) & 15) == 0 &&
+           tc.own[w] == pr.me;
 }
 
 // Issue the even-aligned x windows of a cached tile into xs with TMA bulk
 // copies; every tile arrives once on xbar (list-mode and past-the-end tiles
 // with 0 bytes) so the barrier's phases count tiles.
-__device__ __forceinline__ void issue_x_cached(const double *x, const TileCache &tc, double *xs,
-                                              uint64_t *xbar) {
+template <bool kPeer>
+__device__ __forceinline__ void issue_x_cached(const Peers &pr, const double *x, const TileCache &tc,
+                                              double *xs, uint64_t *xbar) {
     uint32_t bytes = 0;
     for (int w = 0; w < tc.nw; w++)
-        if (tma_window(tc.lo[w], tc.len[w])) bytes += (uint32_t)tc.len[w] * 8;
+        if (tma_ok<kPeer>(pr, x, tc, w)) bytes += (uint32_t)tc.len[w] * 8;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_tx(xbar, bytes);
     for (int w = 0; w < tc.nw; w++)
-        if (tma_window(tc.lo[w], tc.len[w]))
+        if (tma_ok<kPeer>(pr, x, tc, w))
             bulk_load(xs + tc.off[w], x + tc.lo[w], (uint32_t)tc.len[w] * 8, xbar);
 }
 
@@ -244,8 +283,10 @@ __device__ __forceinline__ double fx_value2(uint32_t lo, uint32_t hi, double uns
 }
 
 // kWords: 0 = fp64 shared accumulators (CAS loop per mirror), 2 / 3 =
-// exact-integer fixed point in two / three 32-bit words per slot
-template <int kWords>
+// exact-integer fixed point in two / three 32-bit words per slot.
+// kPeer: multi-GPU peer mode (P.peers); the single-GPU instantiation
+// compiles none of it.
+template <int kWords, bool kPeer>
 __global__ void __launch_bounds__(kThreads, 4)
 k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
     constexpr bool kFixed = kWords > 0;
@@ -284,8 +325,8 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
         s_t[0] = atomicAdd(P.counter, 1);
         s_t[1] = atomicAdd(P.counter, 1);
         s_ex[0] = s_ex[1] = -1100;
-        fetch_tile(P, s_t[0], s_tc[0]);
-        issue_x_cached(x, s_tc[0], xs, &xbar);
+        fetch_tile<kPeer>(P, s_t[0], s_tc[0]);
+        issue_x_cached<kPeer>(P.peers, x, s_tc[0], xs, &xbar);
     }
     long long tprev = clock64();
 #define PHASE(k)                                  \
@@ -314,14 +355,29 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
         // 1. x over the tile's local slots: windows arrived by TMA (issued
         //    during the previous tile's flush), odd-aligned windows and
         //    list-mode slots gathered here
+        const Peers &pr = P.peers;
         if (u0 >= 0) {
             const int32_t *uc = P.ucol + u0;
-            for (int i = tid; i < local; i += kThreads) xs[i] = __ldg(x + __ldg(uc + i));
+            for (int i = tid; i < local; i += kThreads) {
+                const int c = __ldg(uc + i);
+                if (!kPeer) {
+                    xs[i] = __ldg(x + c);
+                } else {
+                    const int64_t g = pr.col_base + c;
+                    const int r = owner_of(pr, g);
+                    xs[i] = r == pr.me ? __ldg(x + c) : pr.x[r][g - pr.bs[r]];
+                }
+            }
         } else {
-            for (int w = 0; w < tc.nw; w++)
-                if (!tma_window(tc.lo[w], tc.len[w]))
-                    for (int i = tid; i < tc.len[w]; i += kThreads)
-                        xs[tc.off[w] + i] = __ldg(x + tc.lo[w] + i);
+            for (int w = 0; w < tc.nw; w++) {
+                if (tma_ok<kPeer>(pr, x, tc, w)) continue;
+                const double *src = x + tc.lo[w];
+                if (kPeer) {
+                    const int r = tc.own[w];
+                    if (r != pr.me) src = pr.x[r] + (pr.col_base + tc.lo[w] - pr.bs[r]);
+                }
+                for (int i = tid; i < tc.len[w]; i += kThreads) xs[tc.off[w] + i] = src[i];
+            }
         }
         mbar_wait(&xbar, (uint32_t)(k & 1), P.watchdog, 5, t);
         asm volatile("cp.async.wait_all;" ::: "memory");  // this tile's record offsets
@@ -337,7 +393,7 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
         __syncthreads();
         PHASE(1);
         if (tid == 0) {
-            fetch_tile(P, s_t[(k + 1) % 3], s_tc[nxt]);  // overlaps the stream
+            fetch_tile<kPeer>(P, s_t[(k + 1) % 3], s_tc[nxt]);  // overlaps the stream
             s_ex[nxt] = -1100;
         }
         int E = 0;
@@ -426,7 +482,7 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
 
         // 3. xs is free: the next tile's x windows and record offsets are
         //    issued first, so they land while this tile flushes
-        if (tid == 0) issue_x_cached(x, s_tc[nxt], xs, &xbar);
+        if (tid == 0) issue_x_cached<kPeer>(P.peers, x, s_tc[nxt], xs, &xbar);
         load_offsets(P, s_tc[nxt].m, s_off[nxt], tid);
         PHASE(4);
 
@@ -455,25 +511,50 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
             for (int i = tid; i < local; i += kThreads) {
                 double a = take(i);
                 const int c = __ldg(uc + i);
-                if (i >= nmsg)
+                double *dst = y + c;
+                bool mine = true;
+                if (kPeer) {  // a column of an earlier rank: its inbox, over NVLink
+                    const int64_t g = pr.col_base + c;
+                    const int r = owner_of(pr, g);
+                    if (r != pr.me) {
+                        dst = pr.y[r] + (g - pr.bs[r]);
+                        mine = false;
+                    }
+                }
+                if (i >= nmsg && mine)  // (a halo row's diagonal belongs to its owner)
                     a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), __ldg(x + c), a);
-                if (a != 0.0) atomicAdd(y + c, a);
+                if (a != 0.0) atomicAdd(dst, a);
             }
         } else {
             for (int w = 0; w < tc.nw; w++) {
                 const int lo = tc.lo[w], len = tc.len[w], off = tc.off[w];
+                // own columns reduce into y; an earlier rank's columns into its
+                // inbox over NVLink (peer mode; their diagonal is the owner's)
+                bool mine = true;
+                double *dst = y + lo;
+                if (kPeer) {
+                    const int r = tc.own[w];
+                    if (r != pr.me) {
+                        mine = false;
+                        dst = pr.y[r] + (pr.col_base + lo - pr.bs[r]);
+                    }
+                }
                 for (int i = tid; i < len; i += kThreads) {
                     const int c = lo + i;
                     double a = take(off + i);
-                    if (c >= r0 && c < r1)
+                    if (mine && c >= r0 && c < r1)
                         a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), __ldg(x + c), a);
-                    if (a != 0.0) atomicAdd(y + c, a);
+                    if (a != 0.0) atomicAdd(dst + i, a);
                 }
             }
         }
         __syncthreads();
         PHASE(3);
     }
+    // peer mode: this CTA's reductions into other GPUs' inboxes are performed
+    // system-wide before the kernel completes (the barrier after the product
+    // is stream-ordered behind it)
+    if (kPeer) __threadfence_system();
     if (P.phase_clk && tid == 0)
         for (int k = 0; k < 6; k++) atomicAdd(P.phase_clk + k, (unsigned long long)s_clk[k]);
 #undef PHASE
@@ -543,6 +624,7 @@ struct pars3_plan {
     unsigned long long *phase_clk = nullptr;
     int32_t *counter = nullptr;
     int64_t bytes = 0;
+    Peers peers{};
 
     ~pars3_plan() {
         void *ptrs[] = {tiles, wins, slice_off, rec, ucol, diag, counter, phase_clk};
@@ -554,7 +636,6 @@ struct pars3_plan {
 extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_options *opt,
                                  int32_t p, const int64_t *block_start, pars3_plan **out,
                                  void *stream) {
-    (void)block_start;
     (void)stream;
     if (!s || !out) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
     *out = nullptr;
@@ -569,6 +650,8 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         if (opt->gap >= 0) o.gap = opt->gap;
         if (opt->mode > 0) o.mode = opt->mode;
         o.skip_empty = (opt->flags & PARS3_PLAN_SKIP_EMPTY) != 0;
+        if ((opt->flags & PARS3_PLAN_CUT_BLOCKS) && block_start && p > 1)
+            for (int32_t r = 1; r < p; r++) o.cuts.push_back((int32_t)block_start[r]);
         if (opt->max_ctas > 0) max_ctas = opt->max_ctas;
     }
     // accumulation of the mirror sums: mode 2 = fp64 shared accumulators,
@@ -655,20 +738,22 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     pl->smem = pl->words == 0 ? Layout<0>::kSmem : pl->words == 2 ? Layout<2>::kSmem : Layout<3>::kSmem;
     // the attribute is per function, shared by every plan: set it to the
     // function's fixed layout size
-    cudaError_t e = cudaFuncSetAttribute(k_tiles<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Layout<0>::kSmem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_tiles<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Layout<2>::kSmem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_tiles<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Layout<3>::kSmem);
+    cudaError_t e = cudaSuccess;
+    {
+        const void *fns[6] = {(const void *)k_tiles<0, false>, (const void *)k_tiles<2, false>,
+                              (const void *)k_tiles<3, false>, (const void *)k_tiles<0, true>,
+                              (const void *)k_tiles<2, true>,  (const void *)k_tiles<3, true>};
+        const int sm[3] = {Layout<0>::kSmem, Layout<2>::kSmem, Layout<3>::kSmem};
+        for (int f = 0; f < 6 && e == cudaSuccess; f++)
+            e = cudaFuncSetAttribute(fns[f], cudaFuncAttributeMaxDynamicSharedMemorySize, sm[f % 3]);
+    }
     int per_sm = 0, sms = 0, dev = 0;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, pl->words == 0 ? k_tiles<0> : pl->words == 2 ? k_tiles<2> : k_tiles<3>, kThreads,
+            &per_sm, pl->words == 0 ? k_tiles<0, false> : pl->words == 2 ? k_tiles<2, false> : k_tiles<3, false>,
+            kThreads,
             pl->smem);
     if (e != cudaSuccess || per_sm < 1) {
         delete pl;
@@ -688,14 +773,43 @@ static int launch_tiles(pars3_plan *pl, const double *x, double *y, bool zero_y,
     CUDA_TRY(cudaMemsetAsync(pl->counter, 0, sizeof(int32_t), st));
     DevPlan P{pl->tiles,      pl->wins,       pl->slice_off, pl->rec,       pl->ucol,
               pl->diag,       pl->counter,    pl->ntiles,    pl->watchdog,  pl->diag_const,
-              pl->diag_alpha, pl->phase_clk,  pl->pf,        pl->pf_dist};
+              pl->diag_alpha, pl->phase_clk,  pl->pf,        pl->pf_dist,  pl->peers};
+    const bool peer = pl->peers.nranks > 0;
     if (pl->words == 0)
-        k_tiles<0><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
+        (peer ? k_tiles<0, true> : k_tiles<0, false>)<<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
     else if (pl->words == 2)
-        k_tiles<2><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
+        (peer ? k_tiles<2, true> : k_tiles<2, false>)<<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
     else
-        k_tiles<3><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
+        (peer ? k_tiles<3, true> : k_tiles<3, false>)<<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
     LAUNCH_CHECK();
+    return PARS3_OK;
+}
+
+extern "C" int pars3_plan_set_peers(pars3_plan *pl, int32_t nranks, int32_t me, int64_t col_base,
+                                    const int64_t *block_start, const uint64_t *x_ptrs,
+                                    const uint64_t *inbox_ptrs) {
+    if (!pl) PARS3_FAIL(PARS3_ERR_ARG, "null plan");
+    if (nranks == 0) {
+        pl->peers = Peers{};
+        return PARS3_OK;
+    }
+    if (nranks < 1 || nranks > kMaxRanks || me < 0 || me >= nranks || !block_start || !x_ptrs ||
+        !inbox_ptrs)
+        PARS3_FAIL(PARS3_ERR_ARG, "peer mode needs 1..%d ranks, a rank id and %d pointers", kMaxRanks,
+                   nranks);
+    if (col_base < 0 || col_base + pl->n > block_start[nranks] || block_start[0] != 0)
+        PARS3_FAIL(PARS3_ERR_ARG, "plan index space [%lld, %lld) outside the blocks",
+                   (long long)col_base, (long long)(col_base + pl->n));
+    Peers pr{};
+    pr.nranks = nranks;
+    pr.me = me;
+    pr.col_base = col_base;
+    for (int r = 0; r <= nranks; r++) pr.bs[r] = block_start[r];
+    for (int r = 0; r < nranks; r++) {
+        pr.x[r] = reinterpret_cast<const double *>(x_ptrs[r]);
+        pr.y[r] = reinterpret_cast<double *>(inbox_ptrs[r]);
+    }
+    pl->peers = pr;
     return PARS3_OK;
 }
 

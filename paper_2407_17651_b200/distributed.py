@@ -49,7 +49,7 @@ import numpy as np
 from .split import BandSplit, PartitionPlan
 
 __all__ = ["RankShard", "shard_for_rank", "split_shard", "exchange_schedule", "DistributedPars3",
-           "emulate_ranks"]
+           "PeerPars3", "emulate_ranks"]
 
 
 @dataclass
@@ -315,6 +315,176 @@ class DistributedPars3:
         """This rank's block of x inside the extended buffer: writing x here
         (e.g. the next iterate of a solver) skips matvec's copy."""
         return self.x_ext[self.shard.own_off:]
+
+
+class _IpcVector:
+    """A float64 device vector in its own cudaMalloc block, exportable to
+    other processes (CUDA IPC), viewed as a torch tensor."""
+
+    def __init__(self, n, device):
+        import ctypes
+
+        import torch
+
+        from . import _lib
+        self._L = _lib.load()
+        self.n = int(n)
+        p = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _lib.check(self._L.pars3_ipc_alloc(8 * max(1, self.n), ctypes.byref(p)), "ipc_alloc")
+        self.ptr = p.value
+        self.device = device
+        self.__cuda_array_interface__ = {"shape": (self.n,), "typestr": "<f8",
+                                         "data": (self.ptr, False), "version": 3}
+        self.tensor = torch.as_tensor(self, device=device)
+
+    def handle(self) -> bytes:
+        import ctypes
+
+        from . import _lib
+        buf = (ctypes.c_uint8 * 64)()
+        _lib.check(self._L.pars3_ipc_handle(ctypes.c_void_p(self.ptr), buf), "ipc_handle")
+        return bytes(buf)
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            self.tensor = None
+            self._L.pars3_ipc_free(ctypes_vp(self.ptr))
+            self.ptr = None
+
+
+def ctypes_vp(v):
+    import ctypes
+    return ctypes.c_void_p(v)
+
+
+class PeerPars3:
+    """One rank's operator in PEER mode: ``y_own = (A x)[lo:hi]`` with the
+    exchange inside the kernel.
+
+    Every rank exports (CUDA IPC) its x block and an inbox for its rows.
+    Its single plan covers the extended range [halo_lo, hi); windows are cut
+    at block boundaries, and the kernel reads an earlier rank's x straight
+    from that rank's buffer and reduces the mirror sums of its rows straight
+    into that rank's inbox (``pars3_plan_set_peers``), over NVLink between
+    GPUs.  A step is: write x, zero y, barrier (every x written, every inbox
+    drained), product, barrier (every reduction landed), y += inbox, drain.
+    The barriers are one-element all-reduces on the current stream (NCCL:
+    device-side, no host sync) or host barriers (gloo tests)."""
+
+    def __init__(self, s: BandSplit, plan: PartitionPlan, group=None, device=None, options=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        from .device import Pars3Operator
+        self.torch, self.dist, self.group = torch, dist, group
+        self.rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        if plan.p != world:
+            raise ValueError(f"plan has {plan.p} blocks but the group has {world} ranks")
+        if world > 8:
+            raise ValueError("peer mode supports up to 8 ranks (one NVLink domain)")
+        if plan.n != s.n or plan.beta != s.beta:
+            raise ValueError(f"plan (n={plan.n}, beta={plan.beta}) does not match "
+                             f"split (n={s.n}, beta={s.beta})")
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.staged = dist.get_backend(group) == "gloo"
+        sh = self.shard = shard_for_rank(s, plan, self.rank)
+        nown = sh.hi - sh.lo
+        # x block and inbox in ONE allocation with one IPC handle: small
+        # cudaMallocs share a VA chunk, and a peer's mapping of one handle
+        # covers only that allocation
+        self._shared = _IpcVector(2 * nown, self.device)
+        self._x = self._shared.tensor[:nown]
+        self._in = self._shared.tensor[nown:]
+        self._shared.tensor.zero_()
+        self.y_own = torch.zeros(nown, dtype=torch.float64, device=self.device)
+        torch.cuda.synchronize(self.device)
+        handles = [None] * world
+        dist.all_gather_object(handles, (self._shared.handle(), nown), group=group)
+        L = _lib.load()
+        self._opened = []
+        xp, ip = [], []
+        for r, (h, nr) in enumerate(handles):
+            if r == self.rank:
+                base = self._shared.ptr
+            else:
+                q = ctypes.c_void_p()
+                buf = (ctypes.c_uint8 * 64).from_buffer_copy(h)
+                with torch.cuda.device(self.device):
+                    _lib.check(L.pars3_ipc_open(buf, ctypes.byref(q)), "ipc_open")
+                self._opened.append(q.value)
+                base = q.value
+            xp.append(base)
+            ip.append(base + 8 * int(nr))
+        # local cut points: every block boundary inside [halo_lo, hi)
+        bs = np.asarray(plan.block_start, dtype=np.int64)
+        cuts = [0] + [int(b - sh.halo_lo) for b in bs[1:-1] if sh.halo_lo < b < sh.hi] + [sh.n_ext]
+        base = tuple(options or ()) + (0, 0, 0, -1, 0, 0, 0)[len(options or ()):]
+        o = base[:5] + (base[5] | _lib.PLAN_CUT_BLOCKS, base[6])
+        e = np.zeros(0, np.int32)
+        self._op = Pars3Operator(sh.n_ext, max(1, sh.n_ext), sh.diags, sh.row_ptr, sh.col_ind,
+                                 sh.off_diags, e, e, np.zeros(0), p=len(cuts) - 1,
+                                 block_start=np.asarray(cuts, dtype=np.int64), device=self.device,
+                                 options=o)
+        self.ops = [self._op]
+        xa = (ctypes.c_uint64 * world)(*xp)
+        ia = (ctypes.c_uint64 * world)(*ip)
+        bsa = np.ascontiguousarray(bs)
+        _lib.check(L.pars3_plan_set_peers(self._op._handle, world, self.rank, sh.halo_lo,
+                                          _lib.ptr(bsa), xa, ia), "plan_set_peers")
+        # the kernel addresses x / y by local index: own block at own_off
+        self._x_local = self._shared.ptr - 8 * sh.own_off
+        self._y_local = self.y_own.data_ptr() - 8 * sh.own_off
+        self._one = torch.zeros(1, dtype=torch.float64, device=self.device)
+
+    def x_view(self):
+        """This rank's x block in the shared buffer (write x here to skip a copy)."""
+        return self._x
+
+    def _barrier(self):
+        if self.staged:
+            self.torch.cuda.synchronize(self.device)
+            self.dist.barrier(group=self.group)
+        else:
+            self.dist.all_reduce(self._one, group=self.group)
+
+    def matvec(self, x_own):
+        from . import _lib
+        sh = self.shard
+        nown = sh.hi - sh.lo
+        if x_own.shape[0] != nown:
+            raise ValueError(f"x block must have {nown} entries, got {x_own.shape[0]}")
+        xb = self._x
+        if x_own.data_ptr() != xb.data_ptr():
+            xb.copy_(x_own)
+        self.y_own.zero_()
+        self._barrier()  # every rank's x is written and its inbox drained
+        _lib.check(self._op._L.pars3_plan_spmv_acc(self._op._handle, self._x_local, self._y_local,
+                                                   _lib.stream_ptr()), "pars3_plan_spmv")
+        self._barrier()  # every mirror reduction into an inbox has landed
+        self.y_own += self._in
+        self._in.zero_()
+        return self.y_own
+
+    def local_product(self):
+        """The rank's kernel alone (no barriers; y accumulates): for timing."""
+        from . import _lib
+        _lib.check(self._op._L.pars3_plan_spmv_acc(self._op._handle, self._x_local, self._y_local,
+                                                   _lib.stream_ptr()), "pars3_plan_spmv")
+
+    def close(self):
+        from . import _lib
+        L = _lib.load()
+        self.torch.cuda.synchronize(self.device)
+        for q in self._opened:
+            L.pars3_ipc_close(ctypes_vp(q))
+        self._opened = []
+        self._op.close()
 
 
 def emulate_ranks(s: BandSplit, plan: PartitionPlan, x, make_local, overlap=False):
