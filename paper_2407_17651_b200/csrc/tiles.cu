@@ -41,13 +41,20 @@ namespace {
 // 4 CTAs per SM x 8 warps (<= 64 registers): 32 warps stream records into
 // registers, and the co-resident CTAs overlap each other's per-tile
 // window/flush phases.
-constexpr int kThreads = 256;
+#ifndef PARS3_THREADS  // build-time shape of the persistent grid (tuning builds)
+#define PARS3_THREADS 256
+#define PARS3_MIN_BLOCKS 4
+#define PARS3_CAP 3200
+#define PARS3_MAX_SLICES 256
+#endif
+constexpr int kThreads = PARS3_THREADS;
+constexpr int kMinBlocks = PARS3_MIN_BLOCKS;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxTileSlices = 256;  // per-tile slice offset table in shared memory
+constexpr int kMaxTileSlices = PARS3_MAX_SLICES;  // per-tile slice offset table in shared memory
 constexpr int kMaxSlots = 8;          // slots per slice (plan seg_max)
 constexpr int kMaxWindowsDev = pars3::kMaxWindows;
-constexpr int kLocalExact = 3200;  // window slots per tile: x + fp64 acc or two words (16 B/slot)
-constexpr int kLocalFixed = 2496;  // x + three uint32 words (20 B/slot)
+constexpr int kLocalExact = PARS3_CAP;  // window slots per tile: x + fp64 acc or two words (16 B/slot)
+constexpr int kLocalFixed = PARS3_CAP == 3200 ? 2496 : PARS3_CAP * 4 / 5 / 32 * 32;  // x + 3 words (20 B/slot)
 constexpr int kTerms2 = 64;        // two-word fixed point: max terms per slot per tile
 // Shared arrays are laid out with a compile-time stride (so the second and
 // third accumulator words are an immediate offset from the first): the
@@ -287,7 +294,7 @@ __device__ __forceinline__ double fx_value2(uint32_t lo, uint32_t hi, double uns
 // kPeer: multi-GPU peer mode (P.peers); the single-GPU instantiation
 // compiles none of it.
 template <int kWords, bool kPeer>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
 k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
     constexpr bool kFixed = kWords > 0;
     constexpr int S = Layout<kWords>::kStride;
@@ -665,6 +672,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     if (o.seg_max > 8) o.seg_max = 8;
     const int32_t want_local = o.local_slots;
     o.local_slots = std::min(want_local, words == 3 ? kLocalFixed : kLocalExact);
+    o.max_segments = std::min(o.max_segments, 32 * kMaxTileSlices);
     o.sink = (uint16_t)(words == 3 ? Layout<3>::kSink : Layout<0>::kSink);
     HostPlan hp;
     int rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
