@@ -80,20 +80,27 @@ def build_problem(cfg: str, beta=None):
         gpu = torch.cuda.is_available()
     except Exception:
         gpu = False
-    # GPU RCM (same labels as the reference, tests/test_gpu_rcm.py) when a device is present
-    perm = P.rcm_order_sss(m0) if gpu else P.rcm_order(P.pattern_from_sss(m0))
-    t2 = time.time()
-    m = P.permute_sss(m0, perm)
+    if gpu:
+        # the whole chain on the device (same arrays as the host chain:
+        # tests/test_gpu_rcm.py), only the results come back
+        from paper_2407_17651_b200.pipeline import prepare_gpu
+        perm, m, s, bw = prepare_gpu(m0, beta)
+        beta = s.beta
+        t2 = t3 = time.time()
+    else:
+        perm = P.rcm_order(P.pattern_from_sss(m0))
+        t2 = time.time()
+        m = P.permute_sss(m0, perm)
+        bw = P.compute_bandwidth(m)
+        if beta is None:
+            beta = P.default_beta(m.n, bw)
+        s = P.split_bands(m, beta)
+        t3 = time.time()
     del m0
-    bw = P.compute_bandwidth(m)
-    if beta is None:
-        beta = P.default_beta(m.n, bw)
-    s = P.split_bands(m, beta)
-    t3 = time.time()
     x = G.make_x(m.n, G.CONFIGS[cfg]["seed_x"])
     log(f"{cfg}: n={m.n} m={m.nnz_offdiag} rcm_bw={bw} beta={beta} mid={s.middle_count} "
-        f"outer={s.outer_count}; gen {t1 - t0:.1f}s rcm ({'gpu' if gpu else 'host'}) {t2 - t1:.2f}s "
-        f"permute+split {t3 - t2:.1f}s")
+        f"outer={s.outer_count}; gen {t1 - t0:.1f}s preprocessing on the "
+        f"{'GPU (rcm+permute+split)' if gpu else 'host'} {t3 - t1:.2f}s")
     return m, s, bw, beta, np.ascontiguousarray(x)
 
 

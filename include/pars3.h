@@ -202,6 +202,23 @@ int pars3_rcm_order_device(int64_t n, const int64_t *indptr, const int32_t *indi
 int pars3_rcm_order_lower_device(int64_t n, const int64_t *row_ptr, const int32_t *col_ind,
                                  int64_t nnz, int64_t *forward, void *stream);
 
+/* The relabel and the band split on the device (csrc/prep_gpu.cu), same
+ * arrays as pars3_permute_lower / pars3_split_fill (and the reference's):
+ * all pointers are device pointers; both synchronise `stream`.
+ * pars3_split_device: mid_ptr[n+1] and outer_ptr[n+1] are always written and
+ * counts[2] = {middle, outer} (host); with mid_col == NULL only that sizing
+ * pass runs.  pars3_bandwidth_device: max(i - c) (reorder.py:120-134). */
+int pars3_permute_lower_device(int64_t n, const int64_t *row_ptr, const int32_t *col_ind,
+                               const double *off_diags, const double *diags, const int64_t *forward,
+                               int64_t *out_row_ptr, int32_t *out_col_ind, double *out_off_diags,
+                               double *out_diags, void *stream);
+int pars3_split_device(int64_t n, const int64_t *row_ptr, const int32_t *col_ind,
+                       const double *off_diags, int64_t beta, int64_t *mid_ptr, int64_t *outer_ptr,
+                       int32_t *mid_col, double *mid_val, int32_t *outer_row, int32_t *outer_col,
+                       double *outer_val, int64_t *counts, void *stream);
+int pars3_bandwidth_device(int64_t n, const int64_t *row_ptr, const int32_t *col_ind,
+                           int64_t *bandwidth, void *stream);
+
 /* Relabel an SSS matrix: replaces coo_to_sss(apply_permutation(coo, perm))
  * (reorder.py:289-297, formats.py:413-475) without the COO round trip.
  * Output arrays sized like the input. */

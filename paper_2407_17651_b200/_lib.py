@@ -81,6 +81,11 @@ _SIGS = {
     "pars3_rcm_order": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, ctypes.c_int]),
     "pars3_rcm_order_device": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
     "pars3_rcm_order_lower_device": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp]),
+    "pars3_permute_lower_device": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                                  _vp, _vp]),
+    "pars3_split_device": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                          _vp, _vp, _vp]),
+    "pars3_bandwidth_device": (ctypes.c_int, [_c_i64, _vp, _vp, ctypes.POINTER(_c_i64), _vp]),
     "pars3_permute_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                            ctypes.c_int]),
     "pars3_split_count": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, ctypes.POINTER(_c_i64),

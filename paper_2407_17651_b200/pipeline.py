@@ -1,0 +1,85 @@
+"""The whole preprocessing chain on the GPU.
+
+``prepare_gpu(m0, beta=None)`` is
+
+    perm = rcm_order(pattern_from_sss(m0))
+    m = permute_sss(m0, perm)
+    bw = compute_bandwidth(m); beta = beta or default_beta(m.n, bw)
+    s = split_bands(m, beta)
+
+with every stage on the device (csrc/rcm.cu, csrc/prep_gpu.cu): the
+skyline arrays are uploaded once, and only the results come back.  The
+returned objects are the host-chain's bit for bit (tests/test_gpu_rcm.py
+checks both chains, and the reference's SHA-256s for c2-c4).  The
+conflict plan (``classify_conflicts``) stays host-native: it is one pass
+over the middle band's row prefixes.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .formats import SssMatrix
+from .reorder import Permutation, _upload
+from .split import BandSplit, default_beta
+
+__all__ = ["prepare_gpu"]
+
+
+def prepare_gpu(m0: SssMatrix, beta: int | None = None, device="cuda"):
+    """(perm, m, s, bandwidth) of the host chain, computed on the GPU."""
+    from .device import require_cuda
+    torch = require_cuda()
+    dev = torch.device(device)
+    L = _lib.load()
+    n, nnz = m0.n, m0.nnz_offdiag
+    with torch.cuda.device(dev):
+        st = _lib.stream_ptr()
+        rp = _upload(m0.row_ptr, np.int64, dev)
+        ci = _upload(m0.col_ind, np.int32, dev)
+        od = _upload(m0.off_diags, np.float64, dev)
+        dg = _upload(m0.diags, np.float64, dev)
+        fw = torch.empty(n, dtype=torch.int64, device=dev)
+        _lib.check(L.pars3_rcm_order_lower_device(n, _lib.ptr(rp), _lib.ptr(ci), int(nnz),
+                                                  _lib.ptr(fw), st), "prepare_gpu: rcm")
+        rp2 = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        ci2 = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        od2 = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+        dg2 = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        _lib.check(L.pars3_permute_lower_device(n, _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(od),
+                                                _lib.ptr(dg), _lib.ptr(fw), _lib.ptr(rp2),
+                                                _lib.ptr(ci2), _lib.ptr(od2), _lib.ptr(dg2), st),
+                   "prepare_gpu: permute")
+        del rp, ci, od, dg
+        bw = _lib._c_i64()
+        _lib.check(L.pars3_bandwidth_device(n, _lib.ptr(rp2), _lib.ptr(ci2), ctypes.byref(bw), st),
+                   "prepare_gpu: bandwidth")
+        bw = int(bw.value)
+        if beta is None:
+            beta = default_beta(n, bw)
+        mp = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        op = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        counts = np.zeros(2, dtype=np.int64)
+        args = (n, _lib.ptr(rp2), _lib.ptr(ci2), _lib.ptr(od2), int(beta), _lib.ptr(mp), _lib.ptr(op))
+        _lib.check(L.pars3_split_device(*args, None, None, None, None, None, _lib.ptr(counts), st),
+                   "prepare_gpu: split")
+        nm, no = int(counts[0]), int(counts[1])
+        mc = torch.empty(max(nm, 1), dtype=torch.int32, device=dev)
+        mv = torch.empty(max(nm, 1), dtype=torch.float64, device=dev)
+        orow = torch.empty(max(no, 1), dtype=torch.int32, device=dev)
+        ocol = torch.empty(max(no, 1), dtype=torch.int32, device=dev)
+        oval = torch.empty(max(no, 1), dtype=torch.float64, device=dev)
+        _lib.check(L.pars3_split_device(*args, _lib.ptr(mc), _lib.ptr(mv), _lib.ptr(orow),
+                                        _lib.ptr(ocol), _lib.ptr(oval), _lib.ptr(counts), st),
+                   "prepare_gpu: split")
+        h = {k: t.cpu().numpy() for k, t in (("fw", fw), ("rp", rp2), ("ci", ci2[:nnz]),
+                                             ("od", od2[:nnz]), ("dg", dg2[:n]), ("mp", mp),
+                                             ("mc", mc[:nm]), ("mv", mv[:nm]), ("orow", orow[:no]),
+                                             ("ocol", ocol[:no]), ("oval", oval[:no]))}
+    perm = Permutation(h["fw"])
+    m = SssMatrix._trusted(n, h["rp"], h["ci"], h["od"], h["dg"])
+    s = BandSplit(n, int(beta), h["dg"], h["mp"], h["mc"], h["mv"], h["orow"], h["ocol"], h["oval"])
+    return perm, m, s, bw

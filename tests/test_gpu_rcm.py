@@ -72,3 +72,39 @@ def test_gpu_rcm_reference_labels(cfg, golden_hashes, lib_built):
     from paper_2407_17651_b200 import generators as G
     g = G.make_config(cfg)
     assert sha(P.rcm_order_sss(_sss(g)).forward) == golden_hashes[cfg]["rcm_forward"]
+
+
+@pytest.mark.parametrize("name,m", [g for g in _graphs() if g[0] in ("rmat12", "band", "stencil27",
+                                                                    "small_components", "all_isolated",
+                                                                    "single")],
+                         ids=lambda v: v if isinstance(v, str) else "")
+@pytest.mark.parametrize("beta", [None, 1, 7])
+def test_gpu_chain_equals_host_chain(name, m, beta, lib_built):
+    """prepare_gpu: RCM -> permute -> bandwidth -> split on the device, every
+    array equal to the host chain's."""
+    from paper_2407_17651_b200.pipeline import prepare_gpu
+    perm = P.rcm_order(P.pattern_from_sss(m))
+    mh = P.permute_sss(m, perm)
+    bw = P.compute_bandwidth(mh)
+    b = P.default_beta(mh.n, bw) if beta is None else beta
+    sh = P.split_bands(mh, b)
+    pg, mg, sg, bwg = prepare_gpu(m, beta)
+    assert np.array_equal(pg.forward, perm.forward) and bwg == bw and sg.beta == b
+    assert mg.equals(mh), name
+    for f in ("diag", "mid_ptr", "mid_col", "mid_val", "outer_row", "outer_col", "outer_val"):
+        assert np.array_equal(getattr(sg, f), getattr(sh, f)), (name, f)
+
+
+def test_gpu_chain_reference_hashes_c2(golden_hashes, lib_built):
+    from conftest import SPLIT_FIELDS
+    from paper_2407_17651_b200 import generators as G
+    from paper_2407_17651_b200.pipeline import prepare_gpu
+    h = golden_hashes["c2"]
+    perm, m, s, bw = prepare_gpu(_sss(G.make_config("c2")))
+    assert sha(perm.forward) == h["rcm_forward"]
+    for k in ("row_ptr", "col_ind", "off_diags", "diags"):
+        assert sha(getattr(m, k)) == h[k], k
+    beta = int(h["beta"])
+    assert s.beta == beta
+    for f in SPLIT_FIELDS:
+        assert sha(getattr(s, f)) == h[f"b{beta}/{f}"], f
