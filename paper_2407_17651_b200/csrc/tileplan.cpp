@@ -49,7 +49,7 @@ struct Built {               // one draft materialised
     std::vector<int32_t> ucol;
     std::vector<int64_t> slice_off;  // relative, bytes
     std::vector<uint8_t> rec;
-    int32_t r0, r1, local, own_loff, max_nslots = 0, max_terms = 0;
+    int32_t r0, r1, local, max_nslots = 0, max_terms = 0;
     int64_t nnz, slots;
     double vmax = 0.0;
 };
@@ -184,7 +184,6 @@ void materialise(const Rows &R, const Draft &d, const PlanOptions &o, Built &b) 
     b.r0 = d.r0;
     b.r1 = d.r1;
     b.local = d.local;
-    b.own_loff = (!d.wlo.empty() && d.r0 >= d.wlo[0]) ? local_of(d, b.wloff, d.r0) : 0;
     b.list = (int)d.wlo.size() > kMaxWindows || d.hub >= 0;
     if (b.list) {
         b.ucol.reserve(d.local);
@@ -284,18 +283,6 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
 #pragma omp parallel for schedule(dynamic, 4)
         for (int64_t t = 0; t < nt; t++) materialise(R, *flat[t], o, built[t]);
 
-        // owner tile of each row: tiles with r1 > r0, ascending r0
-        std::vector<int32_t> own_r0, own_t;
-        for (int64_t t = 0; t < nt; t++)
-            if (built[t].r1 > built[t].r0) {
-                own_r0.push_back(built[t].r0);
-                own_t.push_back((int32_t)t);
-            }
-        auto owner_of = [&](int32_t r) {
-            auto it = std::upper_bound(own_r0.begin(), own_r0.end(), r);
-            return own_t[(size_t)(it - own_r0.begin()) - 1];
-        };
-
         P = HostPlan();
         P.n = n;
         P.tiles.resize(nt);
@@ -330,34 +317,20 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
             m.s0 = (int32_t)s_off[t];
             m.s1 = (int32_t)s_off[t + 1];
             m.local = b.local;
-            m.own_loff = b.own_loff;
+            m.pad0 = m.pad1 = m.pad2 = 0;
             m.u0 = b.list ? (int32_t)u_off[t] : -1;
-            m.wt_lo = INT32_MAX;
-            m.wt_hi = -1;
             {
                 int e = -1074;
                 if (b.vmax > 0.0) std::frexp(b.vmax, &e);  // vmax < 2^e
                 m.ev = e;
             }
-            if (b.list) {
-                std::memcpy(&P.ucol[u_off[t]], b.ucol.data(), b.ucol.size() * sizeof(int32_t));
-                for (size_t w = 0; w < b.wlo.size(); w++) {
-                    int32_t lo = b.wlo[w], hi = b.wlo[w] + b.wlen[w] - 1;
-                    // own rows are the tail of the slot list; exclude them
-                    if (b.r1 > b.r0) hi = std::min(hi, b.r0 - 1);
-                    if (hi < lo) continue;
-                    m.wt_lo = std::min(m.wt_lo, owner_of(lo));
-                    m.wt_hi = std::max(m.wt_hi, owner_of(hi));
-                }
-            }
+            if (b.list) std::memcpy(&P.ucol[u_off[t]], b.ucol.data(), b.ucol.size() * sizeof(int32_t));
             for (size_t w = 0; !b.list && w < b.wlo.size(); w++) {
                 Window &W = P.wins[w_off[t] + w];
                 W.lo = b.wlo[w];
                 W.len = b.wlen[w];
                 W.loff = b.wloff[w];
-                W.t_lo = owner_of(b.wlo[w]);
-                W.t_hi = owner_of(b.wlo[w] + b.wlen[w] - 1);
-                W.pad0 = W.pad1 = W.pad2 = 0;
+                W.pad0 = 0;
             }
             for (size_t s = 0; s < b.slice_off.size(); s++)
                 P.slice_off[s_off[t] + s] = (v_off[t] + b.slice_off[s]) / 16;

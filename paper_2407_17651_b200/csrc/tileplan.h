@@ -41,15 +41,13 @@ struct TileMeta {      // 12 x int32
     int32_t u0;        // offset of the explicit column list (list mode), else -1
     int32_t s0, s1;    // slice range
     int32_t local;     // local index space size
-    int32_t own_loff;  // local index of row r0 (valid when r1 > r0)
-    int32_t wt_lo, wt_hi;  // list mode: hull of owner tiles of non-own slots (wt_lo > wt_hi: none)
+    int32_t pad0, pad1, pad2;
     int32_t ev;        // max |value| of the tile's entries < 2^ev (fixed-point scale)
 };
 
-struct Window {       // 8 x int32
+struct Window {       // 4 x int32
     int32_t lo, len, loff;
-    int32_t t_lo, t_hi;  // owner tiles of rows [lo, lo+len) (inclusive range)
-    int32_t pad0, pad1, pad2;
+    int32_t pad0;
 };
 
 struct HostPlan {
