@@ -64,7 +64,7 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def build_problem(cfg: str, beta=None):
+def build_problem(cfg: str, beta=None, use_gpu=True):
     """Generator -> pattern -> RCM -> relabel -> split (native pipeline)."""
     import numpy as np
 
@@ -75,11 +75,13 @@ def build_problem(cfg: str, beta=None):
     t1 = time.time()
     m0 = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
     del g
-    try:
-        import torch
-        gpu = torch.cuda.is_available()
-    except Exception:
-        gpu = False
+    gpu = False
+    if use_gpu:
+        try:
+            import torch
+            gpu = torch.cuda.is_available()
+        except Exception:
+            gpu = False
     if gpu:
         # the whole chain on the device (same arrays as the host chain:
         # tests/test_gpu_rcm.py), only the results come back
@@ -161,7 +163,52 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(s, x, n, m, reps_max=10, min_seconds=10.0):
+def cpu_baseline_isolated(s, x, n, m, mat, bw):
+    """cpu_baseline in a fresh process (a separate process, so
+    none of this process's CUDA / torch host threads compete with the
+    OpenMP workers -- inside the GPU process the same sample ran 3x slower).
+    The inputs travel through a temporary directory (tmpfs when present)."""
+    import shutil
+    import tempfile
+
+    import numpy as np
+    d = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    try:
+        arrs = {f"s_{k}": getattr(s, k) for k in ("diag", "mid_ptr", "mid_col", "mid_val",
+                                                  "outer_row", "outer_col", "outer_val")}
+        arrs.update({f"m_{k}": getattr(mat, k) for k in ("row_ptr", "col_ind", "off_diags", "diags")})
+        arrs["x"] = x
+        for k, a in arrs.items():
+            np.save(os.path.join(d, k + ".npy"), a)
+        meta = {"n": n, "m": m, "beta": s.beta, "bw": bw}
+        with open(os.path.join(d, "meta.json"), "w") as fh:
+            json.dump(meta, fh)
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-baseline-worker", d],
+                           capture_output=True, text=True, timeout=900)
+        if r.returncode != 0:
+            log(f"cpu baseline worker failed: {r.stderr[-500:]}")
+            return None
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+        out["sample"] += " (separate process)"
+        return out
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+
+
+def cpu_baseline_worker(d):
+    import numpy as np
+
+    import paper_2407_17651_b200 as P
+    meta = json.load(open(os.path.join(d, "meta.json")))
+    ld = lambda k: np.load(os.path.join(d, k + ".npy"))  # noqa: E731
+    s = P.BandSplit(meta["n"], meta["beta"], ld("s_diag"), ld("s_mid_ptr"), ld("s_mid_col"),
+                    ld("s_mid_val"), ld("s_outer_row"), ld("s_outer_col"), ld("s_outer_val"))
+    mat = P.SssMatrix._trusted(meta["n"], ld("m_row_ptr"), ld("m_col_ind"), ld("m_off_diags"),
+                               ld("m_diags"))
+    print(json.dumps(cpu_baseline(s, ld("x"), meta["n"], meta["m"], mat=mat, bw=meta["bw"])))
+
+
+def cpu_baseline(s, x, n, m, reps_max=10, min_seconds=10.0, mat=None, bw=None):
     """The reference algorithm (C restatement of _pars3, parallel.py:60-120)
     on all host cores, p = cores: bounded sample of the same workload."""
     import numpy as np
@@ -181,10 +228,36 @@ def cpu_baseline(s, x, n, m, reps_max=10, min_seconds=10.0):
         O.spmv_pars3(split, plan, x, nthreads=cores)
         times.append(time.perf_counter() - t0)
     mean = sum(times) / len(times)
-    return {"value": algorithmic_bytes(n, m) / mean / 1e9, "unit": "GB/s", "cores": cores,
-            "kind": "port", "sample": f"{len(times)} full SpMVs (oracle C _pars3 restatement, "
-            f"p={cores}, OpenMP {cores} threads), mean {mean * 1e3:.1f} ms",
-            "gflops": algorithmic_flops(n, m) / mean / 1e9, "ms_per_spmv": mean * 1e3}
+    out = {"value": algorithmic_bytes(n, m) / mean / 1e9, "unit": "GB/s", "cores": cores,
+           "kind": "port", "sample": f"{len(times)} full SpMVs (oracle C _pars3 restatement, "
+           f"p={cores}, OpenMP {cores} threads), mean {mean * 1e3:.1f} ms",
+           "gflops": algorithmic_flops(n, m) / mean / 1e9, "ms_per_spmv": mean * 1e3}
+    if mat is not None:
+        # the rest of SURVEY 8(d)'s CPU table, each a bounded sample: the
+        # serial kernel on one core, and pars3 at beta = RCM bandwidth (outer
+        # band empty: the CPU's best case)
+        t0 = time.perf_counter()
+        O.spmv_serial(mat.row_ptr, mat.col_ind, mat.off_diags, mat.diags, x)
+        ts = time.perf_counter() - t0
+        out["serial_1core"] = {"GB/s": algorithmic_bytes(n, m) / ts / 1e9, "ms_per_spmv": ts * 1e3,
+                               "sample": "1 full SpMV (oracle C _spmv_sss restatement, 1 thread)"}
+        if bw is not None and bw != s.beta:
+            import paper_2407_17651_b200 as P
+            sb = P.split_bands(mat, int(bw))
+            split_b = {"n": sb.n, "beta": sb.beta, "mid_ptr": sb.mid_ptr,
+                       "mid_col": sb.mid_col.astype(np.int64), "mid_val": sb.mid_val,
+                       "diag": sb.diag, "outer_row": sb.outer_row.astype(np.int64),
+                       "outer_col": sb.outer_col.astype(np.int64), "outer_val": sb.outer_val}
+            plan_b = O.classify_conflicts(split_b, O.partition_rows(sb.n, cores))
+            O.spmv_pars3(split_b, plan_b, x, nthreads=cores)
+            t0 = time.perf_counter()
+            for _ in range(3):
+                O.spmv_pars3(split_b, plan_b, x, nthreads=cores)
+            tb = (time.perf_counter() - t0) / 3
+            out["pars3_beta_bandwidth"] = {"GB/s": algorithmic_bytes(n, m) / tb / 1e9,
+                                           "ms_per_spmv": tb * 1e3, "beta": int(bw),
+                                           "sample": f"3 full SpMVs, p={cores}, outer band empty"}
+    return out
 
 
 def run_reference(args):
@@ -192,7 +265,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    m, s, bw, beta, x = build_problem(args.config, args.beta)
+    # host-native chain (bit-identical inputs), no CUDA in the reference arm
+    m, s, bw, beta, x = build_problem(args.config, args.beta, use_gpu=False)
     import numpy as np
 
     from oracle import oracle as O
@@ -407,7 +481,7 @@ def run_gpu(args):
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(s, x_host, n, nnz)
+        cpu = cpu_baseline_isolated(s, x_host, n, nnz, m, bw)
     out = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
@@ -457,7 +531,11 @@ def main():
     ap.add_argument("--impl", default="pars3", choices=["pars3", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--cpu-baseline-worker", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cpu_baseline_worker:
+        cpu_baseline_worker(args.cpu_baseline_worker)
+        return
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")
         args.warmup = 3
