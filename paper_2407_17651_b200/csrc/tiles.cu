@@ -389,10 +389,14 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
         mbar_wait(&xbar, (uint32_t)(k & 1), P.watchdog, 5, t);
         asm volatile("cp.async.wait_all;" ::: "memory");  // this tile's record offsets
         if (kFixed) {  // tile-wide bound on |x|: max binary exponent over the slots
+            // |x| < 2^(be - 1022) for normal x; slots in pairs (16-byte loads)
             int e = -1100;
-            for (int i = tid; i < local; i += kThreads) {
-                const int be = (int)((__double_as_longlong(xs[i]) >> 52) & 0x7FF);
-                e = max(e, be - 1022);  // |x| < 2^(be - 1022) for normal x
+            const double2 *xs2 = reinterpret_cast<const double2 *>(xs);
+            for (int i = tid; i < (local + 1) / 2; i += kThreads) {
+                const double2 v = xs2[i];  // (an odd tail's mate is inside the stride, not counted)
+                const int b0 = (int)((__double_as_longlong(v.x) >> 52) & 0x7FF);
+                const int b1 = 2 * i + 1 < local ? (int)((__double_as_longlong(v.y) >> 52) & 0x7FF) : 0;
+                e = max(e, max(b0, b1) - 1022);
             }
             e = __reduce_max_sync(0xffffffffu, e);
             if (lane == 0) atomicMax(&s_ex[cur], e);
