@@ -347,7 +347,8 @@ def run_gpu(args):
         if dop is None:
             dop = DistributedPars3(s, plan, max_ctas=int(os.environ.get("PARS3_MAX_CTAS", "0")))
         op = dop._op  # the dominant product (interior rows in nccl mode)
-        launches_per_step = sum(o.kernel_count(with_dot=False) for o in dop.ops) + 1  # + k_dot
+        # + k_dot (nccl mode) or the fused epilogue k_peer_finish (peer mode)
+        launches_per_step = sum(o.kernel_count(with_dot=False) for o in dop.ops) + 1
         stats = op.stats()
         stats["boundary_entries"] = dop.ops[1].stats()["entries"] if len(dop.ops) > 1 else 0
         stats["dist_mode"] = dist_mode
@@ -361,8 +362,11 @@ def run_gpu(args):
         if dist is None:
             y, d = op.matvec_dot(x, None, y=ybuf, dot=dot)
             return y
-        y = dop.matvec(x)
-        P.device.dot(y, y, out=dot)
+        if hasattr(dop, "local_product"):  # peer mode: the dot comes from the epilogue pass
+            y = dop.matvec(x, dot=dot)
+        else:
+            y = dop.matvec(x)
+            P.device.dot(y, y, out=dot)
         dist.all_reduce(dot)
         return y
 

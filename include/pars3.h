@@ -114,6 +114,12 @@ int pars3_plan_set_peers(pars3_plan *plan, int32_t nranks, int32_t me, int64_t c
                          const int64_t *block_start, const uint64_t *x_ptrs,
                          const uint64_t *inbox_ptrs);
 
+/* Peer-mode step epilogue (one pass): y_out = acc + inbox, acc = inbox = 0,
+ * and, when dot != NULL, *dot = <y_out, y_out> (device scalar; the caller
+ * all-reduces it for the MRS step). */
+int pars3_peer_finish(int64_t n, double *acc, double *inbox, double *y_out, double *dot,
+                      void *stream);
+
 /* Device memory shareable across processes (CUDA IPC) for peer mode:
  * allocate, export a 64-byte handle, open a peer's handle (mapped into this
  * device's address space; P2P access over NVLink when on another GPU),

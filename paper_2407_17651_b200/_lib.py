@@ -60,6 +60,7 @@ _SIGS = {
     "pars3_plan_spmv": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "pars3_plan_spmv_acc": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "pars3_plan_set_peers": (ctypes.c_int, [_vp, _c_i32, _c_i32, _c_i64, _vp, _vp, _vp]),
+    "pars3_peer_finish": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp]),
     "pars3_ipc_alloc": (ctypes.c_int, [_c_i64, ctypes.POINTER(_vp)]),
     "pars3_ipc_free": (ctypes.c_int, [_vp]),
     "pars3_ipc_handle": (ctypes.c_int, [_vp, _vp]),

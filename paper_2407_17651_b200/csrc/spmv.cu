@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <string>
 
 #include "common.h"
@@ -112,5 +113,48 @@ extern "C" int pars3_ipc_open(const uint8_t *handle64, void **ptr) {
 
 extern "C" int pars3_ipc_close(void *ptr) {
     if (ptr) CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+    return PARS3_OK;
+}
+
+// ---- peer-mode step epilogue --------------------------------------------------
+// y_out = acc + inbox, acc = inbox = 0, and (dot != NULL) *dot += <y_out, y_out>:
+// the own-row accumulator, the partials the other ranks reduced into this
+// rank's inbox, both cleared for the next product, and the MRS step's inner
+// product -- one pass instead of four.
+namespace {
+__global__ void __launch_bounds__(512) k_peer_finish(int64_t n, double *__restrict__ acc,
+                                                     double *__restrict__ inbox,
+                                                     double *__restrict__ y_out, double *dot) {
+    double s = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double v = acc[i] + inbox[i];
+        acc[i] = 0.0;
+        inbox[i] = 0.0;
+        y_out[i] = v;
+        s = fma(v, v, s);
+    }
+    if (!dot) return;
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __shared__ double ws[16];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) atomicAdd(dot, s);
+    }
+}
+}  // namespace
+
+extern "C" int pars3_peer_finish(int64_t n, double *acc, double *inbox, double *y_out, double *dot,
+                                 void *stream) {
+    if (n < 0 || (n > 0 && (!acc || !inbox || !y_out))) PARS3_FAIL(PARS3_ERR_ARG, "bad argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dot) CUDA_TRY(cudaMemsetAsync(dot, 0, sizeof(double), st));
+    if (n == 0) return PARS3_OK;
+    const int64_t blocks = std::min<int64_t>((n + 511) / 512, 148 * 4);
+    k_peer_finish<<<(int)blocks, 512, 0, st>>>(n, acc, inbox, y_out, dot);
+    LAUNCH_CHECK();
     return PARS3_OK;
 }

@@ -402,6 +402,9 @@ class PeerPars3:
         self._x = self._shared.tensor[:nown]
         self._in = self._shared.tensor[nown:]
         self._shared.tensor.zero_()
+        # the kernel accumulates the own rows into y_acc (zero between
+        # products); the step epilogue writes y_own = y_acc + inbox
+        self.y_acc = torch.zeros(nown, dtype=torch.float64, device=self.device)
         self.y_own = torch.zeros(nown, dtype=torch.float64, device=self.device)
         torch.cuda.synchronize(self.device)
         handles = [None] * world
@@ -439,7 +442,7 @@ class PeerPars3:
                                           _lib.ptr(bsa), xa, ia), "plan_set_peers")
         # the kernel addresses x / y by local index: own block at own_off
         self._x_local = self._shared.ptr - 8 * sh.own_off
-        self._y_local = self.y_own.data_ptr() - 8 * sh.own_off
+        self._y_local = self.y_acc.data_ptr() - 8 * sh.own_off
         self._one = torch.zeros(1, dtype=torch.float64, device=self.device)
 
     def x_view(self):
@@ -453,7 +456,9 @@ class PeerPars3:
         else:
             self.dist.all_reduce(self._one, group=self.group)
 
-    def matvec(self, x_own):
+    def matvec(self, x_own, dot=None):
+        """y_own = (A x)[lo:hi]; with ``dot`` (a 1-element device tensor) also
+        its local <y_own, y_own>, from the same epilogue pass."""
         from . import _lib
         sh = self.shard
         nown = sh.hi - sh.lo
@@ -462,13 +467,14 @@ class PeerPars3:
         xb = self._x
         if x_own.data_ptr() != xb.data_ptr():
             xb.copy_(x_own)
-        self.y_own.zero_()
         self._barrier()  # every rank's x is written and its inbox drained
-        _lib.check(self._op._L.pars3_plan_spmv_acc(self._op._handle, self._x_local, self._y_local,
-                                                   _lib.stream_ptr()), "pars3_plan_spmv")
+        L = self._op._L
+        _lib.check(L.pars3_plan_spmv_acc(self._op._handle, self._x_local, self._y_local,
+                                         _lib.stream_ptr()), "pars3_plan_spmv")
         self._barrier()  # every mirror reduction into an inbox has landed
-        self.y_own += self._in
-        self._in.zero_()
+        _lib.check(L.pars3_peer_finish(nown, _lib.ptr(self.y_acc), _lib.ptr(self._in),
+                                       _lib.ptr(self.y_own), _lib.ptr(dot) if dot is not None else None,
+                                       _lib.stream_ptr()), "pars3_peer_finish")
         return self.y_own
 
     def local_product(self):

@@ -52,7 +52,11 @@ def _worker(rank, world, port, name, beta, out):
         y1 = op.matvec(xb).clone()
         op.x_view().copy_(xb)          # the zero-copy entry: x written in place
         y2 = op.matvec(op.x_view()).clone()
+        d = torch.zeros(1, dtype=torch.float64, device="cuda")
+        y3 = op.matvec(xb, dot=d)  # the fused epilogue's local <y, y>
         torch.cuda.synchronize()
+        assert abs(float(d) - float(y3 @ y3)) <= 1e-12 * max(1.0, float(y3 @ y3))
+        assert torch.equal(y3, y1) or float((y3 - y1).abs().max()) <= 1e-13
         sizes = np.diff(plan.block_start)
         width = int(sizes.max())
         for yk in (y1, y2):
