@@ -149,6 +149,14 @@ int pars3_plan_spmv_dot(pars3_plan *plan, const double *x, double *y, const doub
  * inner product of a distributed MRS step before its all-reduce. */
 int pars3_dot(int64_t n, const double *a, const double *b, double *out, void *stream);
 
+/* Status of the plan's last product (synchronises `stream`): bit 0 set when
+ * some tile met x values the exact fixed-point accumulation cannot carry
+ * (non-finite, subnormal, or beyond 2^+-900 against the values); the product
+ * is then not exact and the caller redoes it with an fp64-accumulator plan
+ * (mode 2), as the blocking Python entry points do.  Non-finite or extreme
+ * matrix VALUES already select fp64 accumulators at plan creation. */
+int pars3_plan_status(pars3_plan *plan, int32_t *flags, void *stream);
+
 /* Number of libpars3 kernels one pars3_plan_spmv (with_dot = 0) or
  * pars3_plan_spmv_dot (with_dot = 1) call launches (memsets excluded). */
 int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *count);

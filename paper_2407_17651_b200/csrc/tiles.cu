@@ -21,6 +21,7 @@
 // (pars3_plan_spmv_acc).
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -390,12 +391,16 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
         asm volatile("cp.async.wait_all;" ::: "memory");  // this tile's record offsets
         if (kFixed) {  // tile-wide bound on |x|: max binary exponent over the slots
             // |x| < 2^(be - 1022) for normal x; slots in pairs (16-byte loads)
+            // (a subnormal x counts as exponent 1025: the tile is flagged below)
             int e = -1100;
             const double2 *xs2 = reinterpret_cast<const double2 *>(xs);
             for (int i = tid; i < (local + 1) / 2; i += kThreads) {
                 const double2 v = xs2[i];  // (an odd tail's mate is inside the stride, not counted)
-                const int b0 = (int)((__double_as_longlong(v.x) >> 52) & 0x7FF);
-                const int b1 = 2 * i + 1 < local ? (int)((__double_as_longlong(v.y) >> 52) & 0x7FF) : 0;
+                const long long q0 = __double_as_longlong(v.x), q1 = __double_as_longlong(v.y);
+                int b0 = (int)((q0 >> 52) & 0x7FF), b1 = (int)((q1 >> 52) & 0x7FF);
+                if (b0 == 0 && (q0 & 0xFFFFFFFFFFFFFll)) b0 = 2047;
+                if (b1 == 0 && (q1 & 0xFFFFFFFFFFFFFll)) b1 = 2047;
+                if (2 * i + 1 >= local) b1 = 0;
                 e = max(e, max(b0, b1) - 1022);
             }
             e = __reduce_max_sync(0xffffffffu, e);
@@ -411,7 +416,12 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
         double scale = 0.0, unscale = 0.0;
         if (kFixed) {
             E = tc.m.ev + s_ex[cur] + 3;
-            E = max(-1000, min(1000, E));
+            // non-finite or subnormal x, or magnitudes the 2^(50-E) scale
+            // cannot carry: the tile's result is not exact -- raise the
+            // plan's status flag (the blocking entry points then redo the
+            // product with the fp64 kernel, pars3_plan_status)
+            if (tid == 0 && (E > 960 || (E < -960 && s_ex[cur] > -1022))) atomicOr(P.counter + 1, 1);
+            E = max(-960, min(960, E));
             scale = ldexp(1.0, 50 - E);
             unscale = ldexp(1.0, E - 50);
         }
@@ -644,6 +654,22 @@ struct pars3_plan {
     }
 };
 
+// fixed-point accumulation needs finite values in [2^-900, 2^900] (or 0)
+static bool values_fixed_point_safe(const pars3_split_view *s) {
+    const int64_t nm = s->mid_ptr ? s->mid_ptr[s->n] : 0;
+    bool ok = true;
+    auto check = [&](const double *v, int64_t k) {
+#pragma omp parallel for reduction(&& : ok)
+        for (int64_t i = 0; i < k; i++) {
+            const double a = std::fabs(v[i]);
+            ok = ok && (a == 0.0 || (a >= 0x1p-900 && a <= 0x1p900));
+        }
+    };
+    if (nm > 0) check(s->mid_val, nm);
+    if (s->outer_count > 0) check(s->outer_val, s->outer_count);
+    return ok;
+}
+
 extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_options *opt,
                                  int32_t p, const int64_t *block_start, pars3_plan **out,
                                  void *stream) {
@@ -672,6 +698,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     // three words when most tiles are unstructured list tiles
     const int req_mode = opt ? opt->mode : 0;
     int words = req_mode == 1 ? 3 : req_mode == 2 ? 0 : 2;
+    if (words && !values_fixed_point_safe(s)) words = 0;  // fp64 accumulators keep IEEE semantics
     // the shared-memory budget (x + accumulators per slot, 4 CTAs / SM) caps both
     if (o.seg_max > 8) o.seg_max = 8;
     const int32_t want_local = o.local_slots;
@@ -743,7 +770,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     UP(ucol, hp.ucol);
     if (!pl->diag_const) UP(diag, diag);
 #undef UP
-    if (cudaMalloc((void **)&pl->counter, sizeof(int32_t)) != cudaSuccess) {
+    if (cudaMalloc((void **)&pl->counter, 2 * sizeof(int32_t)) != cudaSuccess) {  // claims, status
         delete pl;
         PARS3_FAIL(PARS3_ERR_CUDA, "cudaMalloc failed");
     }
@@ -782,7 +809,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
 static int launch_tiles(pars3_plan *pl, const double *x, double *y, bool zero_y, cudaStream_t st) {
     if (zero_y && pl->n > 0) CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)pl->n, st));
     if (pl->ntiles == 0) return PARS3_OK;
-    CUDA_TRY(cudaMemsetAsync(pl->counter, 0, sizeof(int32_t), st));
+    CUDA_TRY(cudaMemsetAsync(pl->counter, 0, 2 * sizeof(int32_t), st));
     DevPlan P{pl->tiles,      pl->wins,       pl->slice_off, pl->rec,       pl->ucol,
               pl->diag,       pl->counter,    pl->ntiles,    pl->watchdog,  pl->diag_const,
               pl->diag_alpha, pl->phase_clk,  pl->pf,        pl->pf_dist,  pl->peers};
@@ -859,6 +886,16 @@ extern "C" int pars3_dot(int64_t n, const double *a, const double *b, double *ou
     if (((uintptr_t)a | (uintptr_t)b) & 15) PARS3_FAIL(PARS3_ERR_ARG, "a and b must be 16-byte aligned");
     k_dot<<<148 * 4, 512, 0, st>>>((int32_t)n, a, b, out);
     LAUNCH_CHECK();
+    return PARS3_OK;
+}
+
+extern "C" int pars3_plan_status(pars3_plan *pl, int32_t *flags, void *stream) {
+    if (!pl || !flags) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
+    *flags = 0;
+    if (!pl->counter) return PARS3_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemcpyAsync(flags, pl->counter + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
     return PARS3_OK;
 }
 

@@ -259,3 +259,42 @@ def test_host_pipeline_non_blocking(oracle):
         assert rel_err(o.numpy(), y_ref) <= TOL
     y = P.spmv_pars3(s, plan, xs[0])  # blocking; y's cross-tile reductions are unordered
     assert not y.is_cuda and rel_err(y.numpy(), outs[0].numpy()) <= TOL
+
+
+def test_nonfinite_and_extreme_inputs(oracle):
+    """x with inf / nan / subnormal / huge entries, and matrices with extreme
+    values: the blocking entry points return the IEEE result of the
+    reference's arithmetic (the fixed-point kernel flags such tiles and the
+    product is redone with fp64 accumulators)."""
+    import warnings
+
+    from paper_2407_17651_b200 import generators as G
+    g = G.stencil27(12, seed_val=3, alpha=0.5)
+    m, s, plan = _pipeline(g)
+    base = G.make_x(m.n, 5)
+    cases = {}
+    x = base.copy(); x[7] = np.inf; cases["inf"] = x
+    x = base.copy(); x[100] = np.nan; cases["nan"] = x
+    x = base.copy(); x[::3] *= 1e-310; cases["subnormal"] = x
+    x = base.copy() * 1e290; cases["huge"] = x
+    x = base.copy() * 1e-290; cases["tiny"] = x
+    for name, x in cases.items():
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)
+            y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x)
+        y = P.spmv_pars3(s, plan, x)
+        fin = np.isfinite(y_ref)
+        assert np.array_equal(np.isnan(y), np.isnan(y_ref)), name
+        assert np.array_equal(np.isinf(y), np.isinf(y_ref)), name
+        assert np.array_equal(y[np.isinf(y)], y_ref[np.isinf(y_ref)]), name
+        scale = max(np.max(np.abs(y_ref[fin])), np.finfo(float).tiny)
+        assert np.max(np.abs(y[fin] - y_ref[fin])) <= 1e-12 * max(1.0, scale) if scale >= 1 else \
+            np.max(np.abs(y[fin] - y_ref[fin])) <= 1e-12 * scale, name
+    # extreme matrix values select fp64 accumulators at plan creation
+    big = P.SssMatrix(m.n, m.row_ptr, m.col_ind, m.off_diags * 1e295, m.diags)
+    sb = P.split_bands(big, s.beta)
+    pb, _ = P.classify_conflicts(sb, P.partition_rows(m.n, 2))
+    y = P.spmv_pars3(sb, pb, base)
+    y_ref = oracle.spmv_serial(big.row_ptr, big.col_ind, big.off_diags, big.diags, base)
+    assert np.max(np.abs(y - y_ref)) <= 1e-12 * np.max(np.abs(y_ref))
+    assert P.prepare(sb, pb).stats()["accum_words"] == 0
