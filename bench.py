@@ -389,6 +389,8 @@ def run_gpu(args):
             y_ref = O.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x_host)
             parity = O.rel_err(yb, y_ref)
             log(f"parity rel_err vs oracle serial: {parity}")
+            if not parity <= 1e-12:  # a fast wrong product is not a bench number
+                raise SystemExit(f"[bench] parity FAILED: rel_err {parity} > 1e-12")
 
     def barrier():
         if dist is not None:

@@ -88,6 +88,19 @@ typedef struct pars3_plan_options {
 
 #define PARS3_PLAN_SKIP_EMPTY 1
 #define PARS3_PLAN_CUT_BLOCKS 4  /* no window straddles block_start[1..p-1] (peer mode) */
+/* Internal locality order: the plan may store P A P^T for a
+ * permutation P of its own (RCM of the graph without the entries no short
+ * cycle supports) and gather x / y through it; the caller's labels do not
+ * change.  Tried automatically when most tiles are unstructured and kept
+ * when it cuts the shared-memory slots by 30 %; LOCALITY tries it on every
+ * plan, NO_LOCALITY never (peer mode implies NO_LOCALITY). */
+#define PARS3_PLAN_LOCALITY 8
+#define PARS3_PLAN_NO_LOCALITY 16
+
+/* The internal locality order a plan may use (host only; for inspection and
+ * tests): forward[split label] = internal label; *dropped = directed edges
+ * the cycle-support filter removed before the RCM layering (may be NULL). */
+int pars3_locality_order(const pars3_split_view *split, int64_t *forward, int64_t *dropped);
 
 /* Build the device plan of a split on the current device: replaces the
  * per-call setup of _pars3 (parallel.py:136-183).  The split's diagonal,
@@ -164,9 +177,10 @@ int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *c
 /* Device bytes held by the plan. */
 int pars3_plan_bytes(const pars3_plan *plan, int64_t *bytes);
 
-/* stats[10] = {tiles, slices, padded slots, stored entries, windows,
+/* stats[13] = {tiles, slices, padded slots, stored entries, windows,
  * max local slots, grid CTAs, device bytes, list-mode tiles, accumulator
- * words (0 = fp64, 2 or 3 = fixed point)}. */
+ * words (0 = fp64, 2 or 3 = fixed point), locality order (0/1), shared-memory
+ * slots over all tiles, edges the locality filter dropped}. */
 int pars3_plan_stats(const pars3_plan *plan, int64_t *stats);
 int pars3_plan_destroy(pars3_plan *plan);
 

@@ -26,13 +26,13 @@ from .reorder import (AdjacencyPattern, Permutation, apply_permutation, compute_
                       pattern_from_coo, pattern_from_sss, permute_sss, rcm_order, rcm_order_sss,
                       read_permutation, write_permutation)
 from .serial import OpCounter, count_ops, spmv_dense, spmv_serial
-from .split import (BandSplit, ConflictReport, PartitionPlan, classify_conflicts,
+from .split import (locality_order, BandSplit, ConflictReport, PartitionPlan, classify_conflicts,
                     conflict_report, default_beta, merge_splits, partition_rows, split_bands)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "AdjacencyPattern", "BandSplit", "MrsResult", "mrs_solve", "ConflictReport", "CooMatrix", "DiagonalError", "OpCounter",
+    "AdjacencyPattern", "BandSplit", "locality_order", "MrsResult", "mrs_solve", "ConflictReport", "CooMatrix", "DiagonalError", "OpCounter",
     "PartitionPlan", "Permutation", "SkewReport", "SkewSymmetryError", "SssMatrix",
     "StructuralError", "apply_permutation", "as_vector", "classify_conflicts",
     "compute_bandwidth", "conflict_report", "coo_normalize", "coo_to_sss", "count_ops",

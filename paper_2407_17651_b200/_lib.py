@@ -48,6 +48,8 @@ class PlanOptions(ctypes.Structure):
 
 PLAN_SKIP_EMPTY = 1
 PLAN_CUT_BLOCKS = 4
+PLAN_LOCALITY = 8      # try the internal locality order on every plan (pars3.h)
+PLAN_NO_LOCALITY = 16  # never use it
 
 
 # name -> (restype, argtypes)
@@ -70,6 +72,7 @@ _SIGS = {
     "pars3_plan_bytes": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i64)]),
     "pars3_dot": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
     "pars3_plan_stats": (ctypes.c_int, [_vp, _vp]),
+    "pars3_locality_order": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, ctypes.POINTER(_c_i64)]),
     "pars3_plan_status": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i32), _vp]),
     "pars3_plan_kernel_count": (ctypes.c_int, [_vp, _c_i32, ctypes.POINTER(_c_i32)]),
     "pars3_plan_destroy": (ctypes.c_int, [_vp]),

@@ -127,6 +127,24 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
         return;
     }
     if (entries == 0 && o.skip_empty) return;  // nothing to deliver
+    if (o.terms_cap > 0 && 4 * (int64_t)(b - a) > o.tile_rows && b - a > 64) {
+        // most references of one column in this row range (+ a second row
+        // segment): halve the range while it would exceed the two-word
+        // accumulator's exact bound, so the plan keeps two words
+        std::vector<int32_t> cols(scratch);
+        std::sort(cols.begin(), cols.end());
+        int32_t run = 0, best = 0;
+        for (size_t i = 0; i < cols.size(); i++) {
+            run = (i > 0 && cols[i] == cols[i - 1]) ? run + 1 : 1;
+            best = std::max(best, run);
+        }
+        if (best + 1 > o.terms_cap) {
+            const int32_t mid = a + (((b - a) / 2 + 31) & ~31);
+            draft_range(R, a, mid, o, out, scratch);
+            draft_range(R, mid, b, o, out, scratch);
+            return;
+        }
+    }
     Draft d;
     d.r0 = a;
     d.r1 = b;

@@ -30,8 +30,10 @@
 #include <new>
 
 #include "common.h"
+#include "locality.h"
 #include "tileplan.h"
 
+using pars3::LocalityOrder;
 using pars3::HostPlan;
 using pars3::PlanOptions;
 using pars3::TileMeta;
@@ -616,6 +618,66 @@ __global__ void __launch_bounds__(512) k_dot(int32_t n, const double *__restrict
     }
 }
 
+// locality order (locality.cpp): xs[j] = x[inv[j]] (gather: the random
+// accesses are L2 reads, the writes stream)
+__global__ void __launch_bounds__(512) k_perm_in(int32_t n, const int32_t *__restrict__ inv,
+                                                 const double *__restrict__ x, double *__restrict__ xs) {
+    const int32_t stride = gridDim.x * blockDim.x;
+    int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; j + 3 * stride < n; j += 4 * stride) {  // four independent gathers in flight
+        int32_t q[4];
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) q[u] = __ldcs(inv + j + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = __ldg(x + q[u]);
+#pragma unroll
+        for (int u = 0; u < 4; u++) __stcs(xs + j + u * stride, v[u]);
+    }
+    for (; j < n; j += stride) __stcs(xs + j, __ldg(x + __ldcs(inv + j)));
+}
+
+// y[i] = (acc ? y[i] : 0) + ys[perm[i]]; with dot: *dot += <y, w> (w == y allowed)
+template <bool kAcc, bool kDot>
+__global__ void __launch_bounds__(512) k_perm_out(int32_t n, const int32_t *__restrict__ perm,
+                                                  const double *__restrict__ ys, double *y,
+                                                  const double *w, double *dot) {
+    const int32_t stride = gridDim.x * blockDim.x;
+    double s = 0.0;
+    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n; i += 4 * stride) {  // four independent gathers in flight
+        int32_t q[4];
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) q[u] = __ldcs(perm + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = ys[q[u]];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int32_t k = i + u * stride;
+            if (kAcc) v[u] += y[k];
+            if (kDot) s = fma(v[u], w == y ? v[u] : w[k], s);
+            y[k] = v[u];
+        }
+    }
+    for (; i < n; i += stride) {
+        double v = ys[__ldcs(perm + i)];
+        if (kAcc) v += y[i];
+        if (kDot) s = fma(v, w == y ? v : w[i], s);
+        y[i] = v;
+    }
+    if (!kDot) return;
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __shared__ double ws[16];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < 16 ? ws[threadIdx.x] : 0.0;
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) atomicAdd(dot, s);
+    }
+}
+
 template <class T>
 int upload(T **dst, const std::vector<T> &src) {
     *dst = nullptr;
@@ -646,9 +708,14 @@ struct pars3_plan {
     int32_t *counter = nullptr;
     int64_t bytes = 0;
     Peers peers{};
+    // internal locality order (locality.cpp): the tiles hold P A P^T, x and
+    // y pass through perm (split label -> internal label) and xs / ys
+    int32_t *perm = nullptr, *iperm = nullptr;
+    double *xs = nullptr, *ys = nullptr;
+    int64_t local_slots = 0, dropped = 0;
 
     ~pars3_plan() {
-        void *ptrs[] = {tiles, wins, slice_off, rec, ucol, diag, counter, phase_clk};
+        void *ptrs[] = {tiles, wins, slice_off, rec, ucol, diag, counter, phase_clk, perm, iperm, xs, ys};
         for (void *q : ptrs)
             if (q) cudaFree(q);
     }
@@ -678,18 +745,19 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     *out = nullptr;
     if (s->n < 0 || s->n >= INT32_MAX || s->beta < 1) PARS3_FAIL(PARS3_ERR_ARG, "bad split header");
     if (p < 1) PARS3_FAIL(PARS3_ERR_ARG, "worker count must be at least 1, got %d", p);
-    PlanOptions o;
-    int32_t max_ctas = 0;
+    PlanOptions o0;
+    int32_t max_ctas = 0, flags = 0;
     if (opt) {
-        if (opt->tile_rows > 0) o.tile_rows = opt->tile_rows;
-        if (opt->local_slots > 0) o.local_slots = opt->local_slots;
-        if (opt->seg_max > 0) o.seg_max = opt->seg_max;
-        if (opt->gap >= 0) o.gap = opt->gap;
-        if (opt->mode > 0) o.mode = opt->mode;
-        o.skip_empty = (opt->flags & PARS3_PLAN_SKIP_EMPTY) != 0;
+        if (opt->tile_rows > 0) o0.tile_rows = opt->tile_rows;
+        if (opt->local_slots > 0) o0.local_slots = opt->local_slots;
+        if (opt->seg_max > 0) o0.seg_max = opt->seg_max;
+        if (opt->gap >= 0) o0.gap = opt->gap;
+        if (opt->mode > 0) o0.mode = opt->mode;
+        o0.skip_empty = (opt->flags & PARS3_PLAN_SKIP_EMPTY) != 0;
         if ((opt->flags & PARS3_PLAN_CUT_BLOCKS) && block_start && p > 1)
-            for (int32_t r = 1; r < p; r++) o.cuts.push_back((int32_t)block_start[r]);
+            for (int32_t r = 1; r < p; r++) o0.cuts.push_back((int32_t)block_start[r]);
         if (opt->max_ctas > 0) max_ctas = opt->max_ctas;
+        flags = opt->flags;
     }
     // accumulation of the mirror sums: mode 2 = fp64 shared accumulators,
     // mode 1 = exact-integer fixed point in three words, mode 3 = two words
@@ -697,30 +765,74 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     // when the plan allows, else fp64 for window-structured matrices and
     // three words when most tiles are unstructured list tiles
     const int req_mode = opt ? opt->mode : 0;
-    int words = req_mode == 1 ? 3 : req_mode == 2 ? 0 : 2;
-    if (words && !values_fixed_point_safe(s)) words = 0;  // fp64 accumulators keep IEEE semantics
+    int words0 = req_mode == 1 ? 3 : req_mode == 2 ? 0 : 2;
+    if (words0 && !values_fixed_point_safe(s)) words0 = 0;  // fp64 accumulators keep IEEE semantics
     // the shared-memory budget (x + accumulators per slot, 4 CTAs / SM) caps both
-    if (o.seg_max > 8) o.seg_max = 8;
-    const int32_t want_local = o.local_slots;
-    o.local_slots = std::min(want_local, words == 3 ? kLocalFixed : kLocalExact);
-    o.max_segments = std::min(o.max_segments, 32 * kMaxTileSlices);
-    o.sink = (uint16_t)(words == 3 ? Layout<3>::kSink : Layout<0>::kSink);
+    if (o0.seg_max > 8) o0.seg_max = 8;
+    const int32_t want_local = o0.local_slots;
+    o0.max_segments = std::min(o0.max_segments, 32 * kMaxTileSlices);
+    auto build = [&](const pars3_split_view *v, PlanOptions &o, int &words, HostPlan &hp) -> int {
+        o = o0;
+        words = words0;
+        o.terms_cap = words == 2 ? kTerms2 : 0;
+        o.local_slots = std::min(want_local, words == 3 ? kLocalFixed : kLocalExact);
+        o.sink = (uint16_t)(words == 3 ? Layout<3>::kSink : Layout<0>::kSink);
+        int rc = pars3::build_tile_plan(v->n, v->mid_ptr, v->mid_col, v->mid_val, v->outer_count,
+                                        v->outer_row, v->outer_col, v->outer_val, o, hp);
+        if (rc) return rc;
+        if (words == 2 && hp.max_terms > kTerms2) {
+            if (req_mode == 3)
+                PARS3_FAIL(PARS3_ERR_ARG, "two-word accumulation needs <= %d terms per slot, plan has %d",
+                           kTerms2, hp.max_terms);
+            words = 0;
+            if (4ll * hp.list_tiles > (int64_t)hp.tiles.size()) {
+                words = 3;
+                o.terms_cap = 0;
+                o.local_slots = std::min(want_local, kLocalFixed);
+                o.sink = (uint16_t)Layout<3>::kSink;
+                hp = HostPlan();
+                rc = pars3::build_tile_plan(v->n, v->mid_ptr, v->mid_col, v->mid_val, v->outer_count,
+                                            v->outer_row, v->outer_col, v->outer_val, o, hp);
+                if (rc) return rc;
+            }
+        }
+        return PARS3_OK;
+    };
+    auto local_of = [](const HostPlan &hp) {
+        int64_t t = 0;
+        for (const TileMeta &m : hp.tiles) t += m.local;
+        return t;
+    };
+    PlanOptions o;
+    int words = 0;
     HostPlan hp;
-    int rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
-                                    s->outer_row, s->outer_col, s->outer_val, o, hp);
+    int rc = build(s, o, words, hp);
     if (rc) return rc;
-    if (words == 2 && hp.max_terms > kTerms2) {
-        if (req_mode == 3)
-            PARS3_FAIL(PARS3_ERR_ARG, "two-word accumulation needs <= %d terms per slot, plan has %d",
-                       kTerms2, hp.max_terms);
-        words = 0;
-        if (4ll * hp.list_tiles > (int64_t)hp.tiles.size()) {
-            words = 3;
-            o.local_slots = std::min(want_local, kLocalFixed);
-            o.sink = (uint16_t)Layout<3>::kSink;
-            rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
-                                        s->outer_row, s->outer_col, s->outer_val, o, hp);
-            if (rc) return rc;
+    int64_t local = local_of(hp);
+    // internal locality order (locality.cpp): tried when most tiles are
+    // unstructured list tiles whose slots hold few entries each, kept when
+    // it cuts the shared-memory slots (= x gathers + y reductions) by 30 %
+    LocalityOrder lo;
+    const bool may_permute = !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_NO_LOCALITY)) && s->n > 1;
+    const bool unstructured = 2ll * hp.list_tiles > (int64_t)hp.tiles.size() && 4 * local > hp.nnz;
+    if (may_permute && (unstructured || (flags & PARS3_PLAN_LOCALITY)) && hp.nnz > 0) {
+        rc = pars3::locality_order(s, lo);
+        if (rc) return rc;
+        pars3_split_view v{s->n, s->beta, lo.diag.data(), lo.row_ptr.data(), lo.col.data(),
+                           lo.val.data(), 0, nullptr, nullptr, nullptr};
+        PlanOptions o2;
+        int words2 = 0;
+        HostPlan hp2;
+        rc = build(&v, o2, words2, hp2);
+        if (rc) return rc;
+        const int64_t local2 = local_of(hp2);
+        if (10 * local2 < 7 * local) {
+            o = o2;
+            words = words2;
+            hp = std::move(hp2);
+            local = local2;
+        } else {
+            lo = LocalityOrder();
         }
     }
     pars3_plan *pl = new (std::nothrow) pars3_plan;
@@ -749,7 +861,10 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
             cudaMemset(pl->phase_clk, 0, 8 * sizeof(unsigned long long));
         }
     }
-    std::vector<double> diag(s->diag, s->diag + s->n);
+    pl->local_slots = local;
+    pl->dropped = lo.dropped;
+    std::vector<double> diag = lo.forward.empty() ? std::vector<double>(s->diag, s->diag + s->n)
+                                                  : std::move(lo.diag);
     pl->diag_const = 1;
     pl->diag_alpha = s->n ? diag[0] : 0.0;
     for (int64_t i = 1; i < s->n && pl->diag_const; i++)
@@ -769,6 +884,18 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     UP(rec, hp.rec);
     UP(ucol, hp.ucol);
     if (!pl->diag_const) UP(diag, diag);
+    if (!lo.forward.empty()) {
+        UP(perm, lo.forward);
+        std::vector<int32_t> inv(lo.forward.size());
+        for (size_t i = 0; i < inv.size(); i++) inv[lo.forward[i]] = (int32_t)i;
+        UP(iperm, inv);
+        if (cudaMalloc((void **)&pl->xs, sizeof(double) * (size_t)pl->n) != cudaSuccess ||
+            cudaMalloc((void **)&pl->ys, sizeof(double) * (size_t)pl->n) != cudaSuccess) {
+            delete pl;
+            PARS3_FAIL(PARS3_ERR_CUDA, "cudaMalloc failed");
+        }
+        pl->bytes += 2 * sizeof(double) * pl->n;
+    }
 #undef UP
     if (cudaMalloc((void **)&pl->counter, 2 * sizeof(int32_t)) != cudaSuccess) {  // claims, status
         delete pl;
@@ -828,6 +955,8 @@ extern "C" int pars3_plan_set_peers(pars3_plan *pl, int32_t nranks, int32_t me, 
                                     const int64_t *block_start, const uint64_t *x_ptrs,
                                     const uint64_t *inbox_ptrs) {
     if (!pl) PARS3_FAIL(PARS3_ERR_ARG, "null plan");
+    if (pl->perm && nranks != 0)
+        PARS3_FAIL(PARS3_ERR_ARG, "peer mode needs a plan without a locality order (PARS3_PLAN_NO_LOCALITY)");
     if (nranks == 0) {
         pl->peers = Peers{};
         return PARS3_OK;
@@ -852,30 +981,48 @@ extern "C" int pars3_plan_set_peers(pars3_plan *pl, int32_t nranks, int32_t me, 
     return PARS3_OK;
 }
 
+// one product through the plan; with a locality order the tiles run on the
+// internal copies xs / ys and the epilogue gathers y (and the dot) back
+static int plan_product(pars3_plan *pl, const double *x, double *y, bool acc, const double *w,
+                        double *dot, cudaStream_t st) {
+    if (dot) CUDA_TRY(cudaMemsetAsync(dot, 0, sizeof(double), st));
+    if (!pl->perm) {
+        int rc = launch_tiles(pl, x, y, !acc, st);
+        if (rc || !dot || pl->n == 0) return rc;
+        // 16-byte loads need 16-byte aligned vectors (torch allocations are)
+        if (((uintptr_t)y | (uintptr_t)w) & 15) PARS3_FAIL(PARS3_ERR_ARG, "y and w must be 16-byte aligned");
+        k_dot<<<148 * 4, 512, 0, st>>>((int32_t)pl->n, y, w, dot);
+        LAUNCH_CHECK();
+        return PARS3_OK;
+    }
+    const int32_t n = (int32_t)pl->n;
+    const int grid = (int)std::min<int64_t>(148 * 4, (pl->n + 511) / 512);
+    k_perm_in<<<grid, 512, 0, st>>>(n, pl->iperm, x, pl->xs);
+    LAUNCH_CHECK();
+    int rc = launch_tiles(pl, pl->xs, pl->ys, true, st);
+    if (rc) return rc;
+    if (acc)
+        (dot ? k_perm_out<true, true> : k_perm_out<true, false>)<<<grid, 512, 0, st>>>(n, pl->perm, pl->ys, y, w, dot);
+    else
+        (dot ? k_perm_out<false, true> : k_perm_out<false, false>)<<<grid, 512, 0, st>>>(n, pl->perm, pl->ys, y, w, dot);
+    LAUNCH_CHECK();
+    return PARS3_OK;
+}
+
 extern "C" int pars3_plan_spmv(pars3_plan *pl, const double *x, double *y, void *stream) {
     if (!pl || (pl->n > 0 && (!x || !y))) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
-    return launch_tiles(pl, x, y, true, (cudaStream_t)stream);
+    return plan_product(pl, x, y, false, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int pars3_plan_spmv_acc(pars3_plan *pl, const double *x, double *y, void *stream) {
     if (!pl || (pl->n > 0 && (!x || !y))) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
-    return launch_tiles(pl, x, y, false, (cudaStream_t)stream);
+    return plan_product(pl, x, y, true, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int pars3_plan_spmv_dot(pars3_plan *pl, const double *x, double *y, const double *w,
                                    double *dot, void *stream) {
     if (!pl || !dot || (pl->n > 0 && (!x || !y || !w))) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
-    cudaStream_t st = (cudaStream_t)stream;
-    int rc = launch_tiles(pl, x, y, true, st);
-    if (rc) return rc;
-    CUDA_TRY(cudaMemsetAsync(dot, 0, sizeof(double), st));
-    if (pl->n > 0) {
-        // 16-byte loads need 16-byte aligned vectors (torch allocations are)
-        if (((uintptr_t)y | (uintptr_t)w) & 15) PARS3_FAIL(PARS3_ERR_ARG, "y and w must be 16-byte aligned");
-        k_dot<<<148 * 4, 512, 0, st>>>((int32_t)pl->n, y, w, dot);
-        LAUNCH_CHECK();
-    }
-    return PARS3_OK;
+    return plan_product(pl, x, y, false, w, dot, (cudaStream_t)stream);
 }
 
 extern "C" int pars3_dot(int64_t n, const double *a, const double *b, double *out, void *stream) {
@@ -901,7 +1048,8 @@ extern "C" int pars3_plan_status(pars3_plan *pl, int32_t *flags, void *stream) {
 
 extern "C" int pars3_plan_kernel_count(const pars3_plan *pl, int32_t with_dot, int32_t *count) {
     if (!pl || !count) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
-    *count = (pl->ntiles > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 1 : 0);
+    *count = pl->perm ? (pl->ntiles > 0 ? 3 : 2)
+                      : (pl->ntiles > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 1 : 0);
     return PARS3_OK;
 }
 
@@ -923,6 +1071,9 @@ extern "C" int pars3_plan_stats(const pars3_plan *pl, int64_t *stats) {
     stats[7] = pl->bytes;
     stats[8] = pl->list_tiles;
     stats[9] = pl->words;
+    stats[10] = pl->perm ? 1 : 0;
+    stats[11] = pl->local_slots;
+    stats[12] = pl->dropped;
     return PARS3_OK;
 }
 

@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from .formats import SssMatrix, StructuralError
 
-__all__ = ["BandSplit", "PartitionPlan", "ConflictReport", "default_beta", "split_bands",
+__all__ = ["locality_order", "BandSplit", "PartitionPlan", "ConflictReport", "default_beta", "split_bands",
            "merge_splits", "partition_rows", "classify_conflicts", "conflict_report"]
 
 
@@ -96,6 +96,28 @@ def split_bands(m: SssMatrix, beta: int) -> BandSplit:
                                   _lib.ptr(mv), _lib.ptr(orow), _lib.ptr(ocol), _lib.ptr(oval)),
                "split_bands")
     return BandSplit(m.n, int(beta), m.diags, mp, mc, mv, orow, ocol, oval)
+
+
+def locality_order(s: BandSplit):
+    """The internal order a device plan may adopt for locality (no reference
+    counterpart; DESIGN.md §3 "locality order"): RCM of the split's graph
+    after dropping the entries that no path of length 2 or 3 supports.
+    Returns ``(Permutation, dropped)`` with ``forward[split label] =
+    internal label`` and the number of directed edges the filter removed.
+    Host-native; the plan applies it inside the product, so the caller's
+    labels never change."""
+    import ctypes
+
+    from .reorder import Permutation
+    L = _lib.load()
+    view = _lib.SplitView(s.n, s.beta, _lib.ptr(s.diag), _lib.ptr(s.mid_ptr), _lib.ptr(s.mid_col),
+                          _lib.ptr(s.mid_val), int(s.outer_col.size), _lib.ptr(s.outer_row),
+                          _lib.ptr(s.outer_col), _lib.ptr(s.outer_val))
+    fw = np.empty(s.n, dtype=np.int64)
+    dropped = ctypes.c_int64()
+    _lib.check(L.pars3_locality_order(ctypes.byref(view), _lib.ptr(fw), ctypes.byref(dropped)),
+               "locality_order")
+    return Permutation(fw), int(dropped.value)
 
 
 def merge_splits(s: BandSplit) -> SssMatrix:

@@ -298,3 +298,41 @@ def test_nonfinite_and_extreme_inputs(oracle):
     y_ref = oracle.spmv_serial(big.row_ptr, big.col_ind, big.off_diags, big.diags, base)
     assert np.max(np.abs(y - y_ref)) <= 1e-12 * np.max(np.abs(y_ref))
     assert P.prepare(sb, pb).stats()["accum_words"] == 0
+
+
+@pytest.mark.parametrize("flags", [0, 8, 16])
+def test_locality_order(flags, oracle):
+    """The plan's internal locality order (PARS3_PLAN_LOCALITY = 8 forces the
+    attempt, NO_LOCALITY = 16 forbids it, 0 = auto): every entry point
+    (overwrite, accumulate, fused dot with w = y and w = x) against the
+    oracle, in the caller's labels."""
+    import torch
+    from paper_2407_17651_b200 import generators as G
+    from paper_2407_17651_b200.device import operator_for_sss
+    cases = [G.random_band(60000, 1024, 16, 0.01, seed_struct=11, seed_perm=12, seed_val=13),
+             G.rmat(12, 16, seed_struct=3, seed_perm=4, seed_val=5),
+             G.stencil27(14, seed_val=6, alpha=0.5)]
+    for g in cases:
+        m0 = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
+        m = P.permute_sss(m0, P.rcm_order(P.pattern_from_sss(m0)))
+        x = G.make_x(m.n, 9)
+        y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x)
+        op = operator_for_sss(m, options=(0, 0, 0, -1, 0, flags, 0))
+        st = op.stats()
+        if flags == 16:
+            assert st["locality_order"] == 0
+        if flags == 8 and g.name.startswith("random_band"):
+            assert st["locality_order"] == 1, st   # the far entries scramble RCM's layering
+        xd = torch.from_numpy(x).cuda()
+        y = op.matvec(xd)
+        assert rel_err(y.cpu().numpy(), y_ref) <= TOL, (g.name, st)
+        y2 = torch.full((m.n,), 0.25, dtype=torch.float64, device="cuda")
+        op.matvec(xd, y2, accumulate=True)
+        assert rel_err(y2.cpu().numpy() - 0.25, y_ref) <= TOL, (g.name, st)
+        y3, dot = op.matvec_dot(xd, None)
+        yh = y3.cpu().numpy()
+        assert rel_err(yh, y_ref) <= TOL
+        assert abs(float(dot.item()) - float(yh @ yh)) <= 1e-12 * float(yh @ yh)
+        _, dot2 = op.matvec_dot(xd, xd)
+        assert abs(float(dot2.item()) - float(x @ yh)) <= 1e-12 * float(np.abs(x) @ np.abs(yh))
+        assert op.kernel_count(True) == (3 if st["locality_order"] else 2)
