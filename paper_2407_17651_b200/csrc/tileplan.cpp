@@ -108,6 +108,67 @@ void cut_windows(const std::vector<int32_t> &cuts, Draft &d) {
     d.wlen.swap(len2);
 }
 
+// Shared-memory bank conflicts of one slot position across the 32 lanes:
+// the mirror terms go to 32-bit words at lidx (banks lidx mod 32), the x
+// reads are 64-bit (two half-warp wavefronts, lidx mod 16).
+int slot_conflicts(const uint16_t *lx, uint16_t sink) {
+    int b32[32] = {0}, b16[16] = {0}, c = 0;
+    for (int l = 0; l < 32; l++) {
+        if (lx[l] == sink) continue;
+        c += (b32[lx[l] & 31]++ > 0) + (b16[lx[l] & 15]++ > 1);
+    }
+    return c;
+}
+
+// The entries of a row segment may sit in any of its slot positions (the
+// row sum and the exact fixed-point mirror sums do not depend on the order).
+// Unstructured tiles put random columns side by side, so the 32 lanes of a
+// slot position often share banks (c3: 25 M of 45 M shared wavefronts were
+// conflicts).  Greedy: fill positions in turn, each lane taking the
+// remaining entry of its segment that adds the fewest conflicts.  Kept only
+// when it beats the stored (ascending-column) order; structured slices
+// (stencils: consecutive rows, consecutive columns) are conflict-free as
+// stored and stay as they are.
+void spread_banks(double *val, uint16_t *lidx, int32_t nslots, int lanes, uint16_t sink) {
+    if (nslots < 2 || nslots > 8 || lanes < 2) return;
+    int before = 0;
+    for (int32_t k = 0; k < nslots; k++) before += slot_conflicts(lidx + (size_t)k * 32, sink);
+    if (before == 0) return;
+    std::vector<double> v2((size_t)nslots * 32);
+    std::vector<uint16_t> x2((size_t)nslots * 32, sink);
+    uint8_t used[32][8] = {{0}};  // seg_max <= 8
+    int after = 0;
+    for (int32_t k = 0; k < nslots; k++) {
+        int b32[32] = {0}, b16[16] = {0};
+        for (int l = 0; l < lanes; l++) {
+            int best = -1, bc = 1 << 30;
+            for (int32_t q = 0; q < nslots; q++) {
+                const uint16_t c = lidx[(size_t)q * 32 + l];
+                if (used[l][q] || c == sink) continue;
+                const int cost = (b32[c & 31] > 0) + (b16[c & 15] > 1);
+                if (cost < bc) {
+                    bc = cost;
+                    best = q;
+                }
+            }
+            if (best < 0) continue;  // the segment is exhausted: padding
+            used[l][best] = 1;
+            const uint16_t c = lidx[(size_t)best * 32 + l];
+            b32[c & 31]++;
+            b16[c & 15]++;
+            after += bc;
+            x2[(size_t)k * 32 + l] = c;
+            v2[(size_t)k * 32 + l] = val[(size_t)best * 32 + l];
+        }
+    }
+    if (after >= before) return;
+    for (int32_t k = 0; k < nslots; k++)
+        for (int l = 0; l < lanes; l++) {
+            lidx[(size_t)k * 32 + l] = x2[(size_t)k * 32 + l];
+            val[(size_t)k * 32 + l] = x2[(size_t)k * 32 + l] == sink ? 0.0 : v2[(size_t)k * 32 + l];
+        }
+}
+
 void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
                  std::vector<Draft> &out, std::vector<int32_t> &scratch) {
     scratch.clear();
@@ -257,6 +318,7 @@ void materialise(const Rows &R, const Draft &d, const PlanOptions &o, Built &b) 
                 b.nnz++;
             }
         }
+        spread_banks(val, lidx, nslots, (int)(s1 - s0), o.sink);
         b.slots += (int64_t)nslots * 32;
     }
     for (int32_t c : terms) b.max_terms = std::max(b.max_terms, c);
