@@ -188,10 +188,12 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
         return;
     }
     if (entries == 0 && o.skip_empty) return;  // nothing to deliver
-    if (o.terms_cap > 0 && 4 * (int64_t)(b - a) > o.tile_rows && b - a > 64) {
-        // most references of one column in this row range (+ a second row
-        // segment): halve the range while it would exceed the two-word
-        // accumulator's exact bound, so the plan keeps two words
+    bool chunk_row = false;  // one row whose own slot alone exceeds the terms cap
+    if (o.terms_cap > 0 && b - a > o.terms_min_rows / 2) {
+        // terms of the busiest slot: references of one column in this row
+        // range plus the segments of its own row (bounded by the longest
+        // row's).  Halve the range while it exceeds the cap, so the plan can
+        // keep the two-word accumulator; a single row is cut into chunks.
         std::vector<int32_t> cols(scratch);
         std::sort(cols.begin(), cols.end());
         int32_t run = 0, best = 0;
@@ -199,11 +201,16 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
             run = (i > 0 && cols[i] == cols[i - 1]) ? run + 1 : 1;
             best = std::max(best, run);
         }
-        if (best + 1 > o.terms_cap) {
-            const int32_t mid = a + (((b - a) / 2 + 31) & ~31);
-            draft_range(R, a, mid, o, out, scratch);
-            draft_range(R, mid, b, o, out, scratch);
-            return;
+        int64_t segs = 0;
+        for (int32_t r = a; r < b; r++) segs = std::max(segs, (R.count(r) + o.seg_max - 1) / o.seg_max);
+        if (best + segs > o.terms_cap) {
+            if (b - a > std::max(1, o.terms_min_rows)) {
+                const int32_t mid = b - a > 64 ? a + (((b - a) / 2 + 31) & ~31) : a + (b - a) / 2;
+                draft_range(R, a, mid, o, out, scratch);
+                draft_range(R, mid, b, o, out, scratch);
+                return;
+            }
+            chunk_row = b - a == 1;
         }
     }
     Draft d;
@@ -214,7 +221,7 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
     // too fragmented for windows: the tile will carry an explicit column
     // list, so do not pay for gap or alignment slots
     if ((int)d.wlo.size() > kMaxWindows) make_windows(scratch, 0, false, R.n, d);
-    if (d.local <= o.local_slots) {
+    if (d.local <= o.local_slots && !chunk_row) {
         out.push_back(std::move(d));
         return;
     }
@@ -228,7 +235,10 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
     // one row wider than the local space: chunk its entries; the first
     // chunk's tile owns the row, the others are helpers (own range empty)
     const int64_t cnt = R.count(a);
-    const int64_t chunk = o.local_slots - 2;
+    // (with a terms cap, the row's own slot takes one term per segment)
+    const int64_t chunk = o.terms_cap > 2 ? std::min<int64_t>(o.local_slots - 2,
+                                                              (int64_t)(o.terms_cap - 2) * o.seg_max)
+                                          : o.local_slots - 2;
     for (int64_t k0 = 0; k0 < cnt; k0 += chunk) {
         Draft h;
         h.r0 = a;

@@ -29,8 +29,11 @@ struct PlanOptions {
     int32_t mode = 0;           // accumulation: 0 auto, 1 fixed point (3 words), 2 fp64,
                                 // 3 fixed point (2 words) (tiles.cu)
     uint16_t sink = kNoSlot;    // local slot that padding lanes / entries point at (> local_slots)
-    int32_t terms_cap = 0;      // > 0: halve row ranges (down to tile_rows / 4) whose busiest
-                                // column would take more accumulator terms than this
+    int32_t terms_cap = 0;      // > 0: halve row ranges whose busiest slot would take more
+                                // accumulator terms than this (down to terms_min_rows rows;
+                                // 1: single long rows are cut into chunks of at most
+                                // terms_cap - 2 segments)
+    int32_t terms_min_rows = 256;
     bool skip_empty = false;    // rows without entries get no own slot (no diagonal term)
     std::vector<int32_t> cuts;  // ascending local indices no window may straddle (peer mode)
 };

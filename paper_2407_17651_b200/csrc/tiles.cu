@@ -775,6 +775,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         o = o0;
         words = words0;
         o.terms_cap = words == 2 ? kTerms2 : 0;
+        if (const char *ts = getenv("PARS3_TERMS_MIN_ROWS")) o.terms_min_rows = atoi(ts);  // tuning knob
         o.local_slots = std::min(want_local, words == 3 ? kLocalFixed : kLocalExact);
         o.sink = (uint16_t)(words == 3 ? Layout<3>::kSink : Layout<0>::kSink);
         int rc = pars3::build_tile_plan(v->n, v->mid_ptr, v->mid_col, v->mid_val, v->outer_count,
