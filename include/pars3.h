@@ -96,6 +96,13 @@ typedef struct pars3_plan_options {
  * plan, NO_LOCALITY never (peer mode implies NO_LOCALITY). */
 #define PARS3_PLAN_LOCALITY 8
 #define PARS3_PLAN_NO_LOCALITY 16
+/* Direct mode: when the tiles would stage about one entry per
+ * shared-memory slot (no reuse, e.g. R-MAT), the plan keeps the entries
+ * row-major and one kernel gathers x and reduces the mirror terms straight
+ * into y (fp64 L2 reductions).  Chosen automatically; DIRECT forces it,
+ * NO_DIRECT forbids it (peer mode and SKIP_EMPTY plans never use it). */
+#define PARS3_PLAN_DIRECT 32
+#define PARS3_PLAN_NO_DIRECT 64
 
 /* The internal locality order a plan may use (host only; for inspection and
  * tests): forward[split label] = internal label; *dropped = directed edges
@@ -177,10 +184,10 @@ int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *c
 /* Device bytes held by the plan. */
 int pars3_plan_bytes(const pars3_plan *plan, int64_t *bytes);
 
-/* stats[13] = {tiles, slices, padded slots, stored entries, windows,
+/* stats[14] = {tiles, slices, padded slots, stored entries, windows,
  * max local slots, grid CTAs, device bytes, list-mode tiles, accumulator
  * words (0 = fp64, 2 or 3 = fixed point), locality order (0/1), shared-memory
- * slots over all tiles, edges the locality filter dropped}. */
+ * slots over all tiles, edges the locality filter dropped, direct mode (0/1)}. */
 int pars3_plan_stats(const pars3_plan *plan, int64_t *stats);
 int pars3_plan_destroy(pars3_plan *plan);
 

@@ -50,6 +50,8 @@ PLAN_SKIP_EMPTY = 1
 PLAN_CUT_BLOCKS = 4
 PLAN_LOCALITY = 8      # try the internal locality order on every plan (pars3.h)
 PLAN_NO_LOCALITY = 16  # never use it
+PLAN_DIRECT = 32       # direct mode (no shared staging) forced (pars3.h)
+PLAN_NO_DIRECT = 64    # never direct mode
 
 
 # name -> (restype, argtypes)

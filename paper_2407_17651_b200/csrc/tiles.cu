@@ -678,6 +678,82 @@ __global__ void __launch_bounds__(512) k_perm_out(int32_t n, const int32_t *__re
     }
 }
 
+// Direct mode (plans whose tiles would hold about one entry per shared
+// slot, e.g. c4's R-MAT): no shared staging.  y = d.x (+ y) first, then
+// every stored entry a_rc gathers x_c into its row's register sum and
+// reduces -a_rc x_r straight into y_c (fp64 red.global.add, L2).  Each lane
+// owns kDirectRun consecutive entries (row-major) and issues all their x
+// gathers at once, so long rows spread over lanes and warps (nnz-balanced),
+// and a lane reduces its row sum once per row run.
+
+__global__ void __launch_bounds__(512) k_direct_init(int32_t n, const double *__restrict__ diag,
+                                                     double alpha, const double *__restrict__ x,
+                                                     double *y, int acc) {
+    const int32_t stride = gridDim.x * blockDim.x;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double d = diag ? diag[i] : alpha;
+        const double v = d * __ldg(x + i);
+        y[i] = acc ? y[i] + v : v;
+    }
+}
+
+template <int kDirectRun>
+__global__ void __launch_bounds__(256) k_direct(int64_t m, const int32_t *__restrict__ row,
+                                                const int32_t *__restrict__ col,
+                                                const double *__restrict__ val,
+                                                const double *__restrict__ x, double *y) {
+    const int64_t nrun = (m + kDirectRun - 1) / kDirectRun;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nrun; t += stride) {
+        const int64_t e0 = t * kDirectRun;
+        int32_t r[kDirectRun], c[kDirectRun];
+        double v[kDirectRun];
+        if (e0 + kDirectRun <= m) {  // 16-byte loads (the arrays are 16-byte aligned, runs of 8)
+            const int4 *r4 = reinterpret_cast<const int4 *>(row + e0);
+            const int4 *c4 = reinterpret_cast<const int4 *>(col + e0);
+            const double2 *v2 = reinterpret_cast<const double2 *>(val + e0);
+#pragma unroll
+            for (int h = 0; h < kDirectRun / 4; h++) {
+                const int4 a = __ldcs(r4 + h), b = __ldcs(c4 + h);
+                r[4 * h] = a.x; r[4 * h + 1] = a.y; r[4 * h + 2] = a.z; r[4 * h + 3] = a.w;
+                c[4 * h] = b.x; c[4 * h + 1] = b.y; c[4 * h + 2] = b.z; c[4 * h + 3] = b.w;
+            }
+#pragma unroll
+            for (int h = 0; h < kDirectRun / 2; h++) {
+                const double2 a = __ldcs(v2 + h);
+                v[2 * h] = a.x;
+                v[2 * h + 1] = a.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kDirectRun; j++) {
+                const bool in = e0 + j < m;
+                r[j] = in ? row[e0 + j] : (j ? r[j - 1] : 0);
+                c[j] = in ? col[e0 + j] : -1;  // -1: past the end
+                v[j] = in ? val[e0 + j] : 0.0;
+            }
+        }
+        double xc[kDirectRun];
+#pragma unroll
+        for (int j = 0; j < kDirectRun; j++) xc[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;  // all in flight
+        int32_t cur = r[0];
+        double xr = __ldg(x + cur), acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < kDirectRun; j++) {
+            if (r[j] != cur) {
+                atomicAdd(y + cur, acc);
+                cur = r[j];
+                xr = __ldg(x + cur);
+                acc = 0.0;
+            }
+            if (c[j] < 0) break;
+            acc = fma(v[j], xc[j], acc);
+            atomicAdd(y + c[j], -v[j] * xr);
+        }
+        atomicAdd(y + cur, acc);
+    }
+}
+
 template <class T>
 int upload(T **dst, const std::vector<T> &src) {
     *dst = nullptr;
@@ -713,9 +789,16 @@ struct pars3_plan {
     int32_t *perm = nullptr, *iperm = nullptr;
     double *xs = nullptr, *ys = nullptr;
     int64_t local_slots = 0, dropped = 0;
+    // direct mode (k_direct): row-major entries, no tiles
+    int32_t direct = 0, direct_run = 16;  // entries per lane: 16 measured best on c4 (4: 1.00 ms,
+                                          // 8: 0.89, 16: 0.83; profiles/r01/sweep_direct_run_c4.txt)
+    int64_t dm = 0;
+    int32_t *drow = nullptr, *dcol = nullptr;
+    double *dval = nullptr;
 
     ~pars3_plan() {
-        void *ptrs[] = {tiles, wins, slice_off, rec, ucol, diag, counter, phase_clk, perm, iperm, xs, ys};
+        void *ptrs[] = {tiles, wins, slice_off, rec, ucol, diag, counter, phase_clk, perm, iperm, xs, ys,
+                        drow, dcol, dval};
         for (void *q : ptrs)
             if (q) cudaFree(q);
     }
@@ -814,7 +897,8 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     // unstructured list tiles whose slots hold few entries each, kept when
     // it cuts the shared-memory slots (= x gathers + y reductions) by 30 %
     LocalityOrder lo;
-    const bool may_permute = !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_NO_LOCALITY)) && s->n > 1;
+    const bool may_permute =
+        !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_NO_LOCALITY | PARS3_PLAN_DIRECT)) && s->n > 1;
     const bool unstructured = 2ll * hp.list_tiles > (int64_t)hp.tiles.size() && 4 * local > hp.nnz;
     if (may_permute && (unstructured || (flags & PARS3_PLAN_LOCALITY)) && hp.nnz > 0) {
         rc = pars3::locality_order(s, lo);
@@ -836,13 +920,48 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
             lo = LocalityOrder();
         }
     }
+    // direct mode: the tiles would stage about one entry per slot (no reuse
+    // of x or of the accumulators in shared memory)
+    const bool direct =
+        lo.forward.empty() && hp.nnz > 0 &&
+        !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_SKIP_EMPTY | PARS3_PLAN_NO_DIRECT)) &&
+        ((flags & PARS3_PLAN_DIRECT) ||
+         (2ll * hp.list_tiles > (int64_t)hp.tiles.size() && 10 * local >= 9 * hp.nnz));
+    std::vector<int32_t> drow, dcol;
+    std::vector<double> dval;
+    if (direct) {  // row-major entries: a row's outer entries, then its middle ones
+        try {
+            const int64_t m = (s->mid_ptr ? s->mid_ptr[s->n] : 0) + s->outer_count;
+            drow.resize(m);
+            dcol.resize(m);
+            dval.resize(m);
+            int64_t o_k = 0, e = 0;
+            for (int64_t i = 0; i < s->n; i++) {
+                for (; o_k < s->outer_count && s->outer_row[o_k] == i; o_k++, e++) {
+                    drow[e] = (int32_t)i;
+                    dcol[e] = s->outer_col[o_k];
+                    dval[e] = s->outer_val[o_k];
+                }
+                for (int64_t k = s->mid_ptr[i]; k < s->mid_ptr[i + 1]; k++, e++) {
+                    drow[e] = (int32_t)i;
+                    dcol[e] = s->mid_col[k];
+                    dval[e] = s->mid_val[k];
+                }
+            }
+            if (e != m) PARS3_FAIL(PARS3_ERR_STRUCT, "outer rows are not sorted");
+        } catch (const std::bad_alloc &) {
+            PARS3_FAIL(PARS3_ERR_NOMEM, "out of host memory");
+        }
+        hp = HostPlan();  // no tiles are uploaded
+        hp.nnz = (int64_t)dval.size();
+    }
     pars3_plan *pl = new (std::nothrow) pars3_plan;
     if (!pl) PARS3_FAIL(PARS3_ERR_NOMEM, "out of host memory");
     pl->n = s->n;
     pl->beta = s->beta;
     pl->p = p;
     pl->ntiles = (int32_t)hp.tiles.size();
-    pl->nslices = (int32_t)hp.slice_off.size() - 1;
+    pl->nslices = std::max<int32_t>(0, (int32_t)hp.slice_off.size() - 1);
     pl->lmax = hp.max_local;
     pl->nnz = hp.nnz;
     pl->slots = hp.slots;
@@ -879,6 +998,15 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         }                                          \
         pl->bytes += sizeof(src[0]) * src.size();  \
     } while (0)
+    if (direct) {
+        pl->direct = 1;
+        if (const char *dr = getenv("PARS3_DIRECT_RUN")) pl->direct_run = atoi(dr);  // tuning knob
+        if (pl->direct_run != 4 && pl->direct_run != 8) pl->direct_run = 16;
+        pl->dm = (int64_t)dval.size();
+        UP(drow, drow);
+        UP(dcol, dcol);
+        UP(dval, dval);
+    }
     UP(tiles, hp.tiles);
     UP(wins, hp.wins);
     UP(slice_off, hp.slice_off);
@@ -898,7 +1026,8 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         pl->bytes += 2 * sizeof(double) * pl->n;
     }
 #undef UP
-    if (cudaMalloc((void **)&pl->counter, 2 * sizeof(int32_t)) != cudaSuccess) {  // claims, status
+    if (cudaMalloc((void **)&pl->counter, 2 * sizeof(int32_t)) != cudaSuccess ||  // claims, status
+        cudaMemset(pl->counter, 0, 2 * sizeof(int32_t)) != cudaSuccess) {
         delete pl;
         PARS3_FAIL(PARS3_ERR_CUDA, "cudaMalloc failed");
     }
@@ -935,6 +1064,22 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
 }
 
 static int launch_tiles(pars3_plan *pl, const double *x, double *y, bool zero_y, cudaStream_t st) {
+    if (pl->direct) {
+        if (pl->n == 0) return PARS3_OK;
+        const int grid = (int)std::min<int64_t>(148 * 4, (pl->n + 511) / 512);
+        k_direct_init<<<grid, 512, 0, st>>>((int32_t)pl->n, pl->diag_const ? nullptr : pl->diag,
+                                            pl->diag_alpha, x, y, zero_y ? 0 : 1);
+        LAUNCH_CHECK();
+        const int run = pl->direct_run;
+        const int64_t runs = (pl->dm + run - 1) / run;
+        const int grid2 = (int)std::min<int64_t>(148 * 16, (runs + 255) / 256);
+        if (grid2 > 0) {
+            auto fn = run == 4 ? k_direct<4> : run == 16 ? k_direct<16> : k_direct<8>;
+            fn<<<grid2, 256, 0, st>>>(pl->dm, pl->drow, pl->dcol, pl->dval, x, y);
+            LAUNCH_CHECK();
+        }
+        return PARS3_OK;
+    }
     if (zero_y && pl->n > 0) CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)pl->n, st));
     if (pl->ntiles == 0) return PARS3_OK;
     CUDA_TRY(cudaMemsetAsync(pl->counter, 0, 2 * sizeof(int32_t), st));
@@ -956,7 +1101,7 @@ extern "C" int pars3_plan_set_peers(pars3_plan *pl, int32_t nranks, int32_t me, 
                                     const int64_t *block_start, const uint64_t *x_ptrs,
                                     const uint64_t *inbox_ptrs) {
     if (!pl) PARS3_FAIL(PARS3_ERR_ARG, "null plan");
-    if (pl->perm && nranks != 0)
+    if ((pl->perm || pl->direct) && nranks != 0)
         PARS3_FAIL(PARS3_ERR_ARG, "peer mode needs a plan without a locality order (PARS3_PLAN_NO_LOCALITY)");
     if (nranks == 0) {
         pl->peers = Peers{};
@@ -1049,8 +1194,11 @@ extern "C" int pars3_plan_status(pars3_plan *pl, int32_t *flags, void *stream) {
 
 extern "C" int pars3_plan_kernel_count(const pars3_plan *pl, int32_t with_dot, int32_t *count) {
     if (!pl || !count) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
-    *count = pl->perm ? (pl->ntiles > 0 ? 3 : 2)
-                      : (pl->ntiles > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 1 : 0);
+    if (pl->direct)
+        *count = (pl->n > 0 ? 1 : 0) + (pl->dm > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 1 : 0);
+    else
+        *count = pl->perm ? (pl->ntiles > 0 ? 3 : 2)
+                          : (pl->ntiles > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 1 : 0);
     return PARS3_OK;
 }
 
@@ -1075,6 +1223,7 @@ extern "C" int pars3_plan_stats(const pars3_plan *pl, int64_t *stats) {
     stats[10] = pl->perm ? 1 : 0;
     stats[11] = pl->local_slots;
     stats[12] = pl->dropped;
+    stats[13] = pl->direct;
     return PARS3_OK;
 }
 

@@ -336,3 +336,42 @@ def test_locality_order(flags, oracle):
         _, dot2 = op.matvec_dot(xd, xd)
         assert abs(float(dot2.item()) - float(x @ yh)) <= 1e-12 * float(np.abs(x) @ np.abs(yh))
         assert op.kernel_count(True) == (3 if st["locality_order"] else 2)
+
+
+@pytest.mark.parametrize("flags", [0, 32, 64])
+def test_direct_mode(flags, oracle):
+    """Direct mode (PARS3_PLAN_DIRECT = 32 forces it, NO_DIRECT = 64 forbids
+    it, 0 = auto): the row-major entries with global gathers and reductions,
+    every entry point, against the oracle; the shifted diagonal (constant and
+    not) included."""
+    import torch
+    from paper_2407_17651_b200 import generators as G
+    from paper_2407_17651_b200.device import operator_for_sss
+    cases = [G.rmat(13, 16, seed_struct=7, seed_perm=8, seed_val=9),
+             G.random_band(30001, 700, 9, 0.03, seed_struct=1, seed_perm=2, seed_val=3),
+             G.stencil27(12, seed_val=6, alpha=0.5), G.grid5(30, seed_perm=7, seed_val=8)]
+    for g in cases:
+        m = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
+        diags = [m.diags, np.linspace(-1.0, 2.0, m.n)]
+        for d in diags:
+            mm = P.SssMatrix._trusted(m.n, m.row_ptr, m.col_ind, m.off_diags, d)
+            x = G.make_x(m.n, 9)
+            y_ref = oracle.spmv_serial(mm.row_ptr, mm.col_ind, mm.off_diags, mm.diags, x)
+            op = operator_for_sss(mm, options=(0, 0, 0, -1, 0, flags, 0))
+            st = op.stats()
+            if flags == 32:
+                assert st["direct"] == 1 and st["tiles"] == 0, st
+            if flags == 64:
+                assert st["direct"] == 0
+            xd = torch.from_numpy(x).cuda()
+            y = op.matvec(xd)
+            assert rel_err(y.cpu().numpy(), y_ref) <= TOL, (g.name, st)
+            y2 = torch.full((m.n,), -1.5, dtype=torch.float64, device="cuda")
+            op.matvec(xd, y2, accumulate=True)
+            assert rel_err(y2.cpu().numpy() + 1.5, y_ref) <= TOL, (g.name, st)
+            y3, dot = op.matvec_dot(xd, None)
+            yh = y3.cpu().numpy()
+            assert abs(float(dot.item()) - float(yh @ yh)) <= 1e-12 * float(yh @ yh)
+            assert op.status() == 0
+            if st["direct"]:
+                assert op.kernel_count(True) == 3
