@@ -842,6 +842,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         if (opt->max_ctas > 0) max_ctas = opt->max_ctas;
         flags = opt->flags;
     }
+    if (const char *ff = getenv("PARS3_FORCE_FLAGS")) flags |= atoi(ff);  // debug / tuning knob
     // accumulation of the mirror sums: mode 2 = fp64 shared accumulators,
     // mode 1 = exact-integer fixed point in three words, mode 3 = two words
     // (needs <= kTerms2 terms per slot and tile), mode 0 = auto: two words
