@@ -922,11 +922,20 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         }
     }
     // direct mode: the tiles would stage about one entry per slot (no reuse
-    // of x or of the accumulators in shared memory)
+    // of x or of the accumulators in shared memory), or a mid-size matrix
+    // whose tiles would leave most of the persistent grid idle (c2: 256
+    // tiles, a latency-bound chain per tile; direct measured 17 % faster)
+    int sms_now = 148;
+    {
+        int dev_now = 0;
+        if (cudaGetDevice(&dev_now) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms_now, cudaDevAttrMultiProcessorCount, dev_now);
+    }
+    const bool few_tiles = (int64_t)hp.tiles.size() < 2ll * sms_now && hp.nnz >= (1 << 19);
     const bool direct =
         lo.forward.empty() && hp.nnz > 0 &&
         !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_SKIP_EMPTY | PARS3_PLAN_NO_DIRECT)) &&
-        ((flags & PARS3_PLAN_DIRECT) ||
+        ((flags & PARS3_PLAN_DIRECT) || few_tiles ||
          (2ll * hp.list_tiles > (int64_t)hp.tiles.size() && 10 * local >= 9 * hp.nnz));
     std::vector<int32_t> drow, dcol;
     std::vector<double> dval;

@@ -335,7 +335,7 @@ def test_locality_order(flags, oracle):
         assert abs(float(dot.item()) - float(yh @ yh)) <= 1e-12 * float(yh @ yh)
         _, dot2 = op.matvec_dot(xd, xd)
         assert abs(float(dot2.item()) - float(x @ yh)) <= 1e-12 * float(np.abs(x) @ np.abs(yh))
-        assert op.kernel_count(True) == (3 if st["locality_order"] else 2)
+        assert op.kernel_count(True) == (3 if st["locality_order"] or st["direct"] else 2)
 
 
 @pytest.mark.parametrize("flags", [0, 32, 64])
