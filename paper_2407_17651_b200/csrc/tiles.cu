@@ -619,7 +619,8 @@ __global__ void __launch_bounds__(512) k_dot(int32_t n, const double *__restrict
 }
 
 // locality order (locality.cpp): xs[j] = x[inv[j]] (gather: the random
-// accesses are L2 reads, the writes stream)
+// accesses are reads, the writes stream; the scatter form xs[perm[i]] = x[i]
+// measured 42 against 22 us on c3)
 __global__ void __launch_bounds__(512) k_perm_in(int32_t n, const int32_t *__restrict__ inv,
                                                  const double *__restrict__ x, double *__restrict__ xs) {
     const int32_t stride = gridDim.x * blockDim.x;
