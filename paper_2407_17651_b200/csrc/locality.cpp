@@ -98,7 +98,10 @@ int locality_order(const pars3_split_view *s, LocalityOrder &out) {
             for (int64_t e = ip[i]; e < ip[i + 1]; e++) work += ip[ix[e] + 1] - ip[ix[e]];
             hub[i] = work > kTwoHopCap;
         }
-#pragma omp parallel
+        // two n-sized scratch arrays per thread: cap the threads at ~2 GB
+        const int nt = (int)std::max<int64_t>(
+            1, std::min<int64_t>(omp_get_max_threads(), (int64_t)(2ll << 30) / (8 * std::max<int64_t>(n, 1))));
+#pragma omp parallel num_threads(nt)
         {
             std::vector<int32_t> stamp(n, -1), cnt(n, 0);
 #pragma omp for schedule(dynamic, 4096)
