@@ -108,3 +108,22 @@ def test_gpu_chain_reference_hashes_c2(golden_hashes, lib_built):
     assert s.beta == beta
     for f in SPLIT_FIELDS:
         assert sha(getattr(s, f)) == h[f"b{beta}/{f}"], f
+
+
+def test_page_locked_download(lib_built):
+    """pipeline._download (page-locked return path of prepare_gpu): every
+    dtype the chain returns, empty and multi-chunk tensors, bytes unchanged."""
+    import torch
+
+    from paper_2407_17651_b200 import pipeline
+    rng = np.random.default_rng(11)
+    hs = [rng.integers(-2**40, 2**40, 3_000_001, dtype=np.int64),
+          rng.integers(-2**31, 2**31 - 1, 20_000_003, dtype=np.int32),  # > one 64 MB chunk
+          rng.uniform(-1, 1, 12_345).astype(np.float64),
+          np.empty(0, dtype=np.float64), np.empty(0, dtype=np.int32)]
+    ds = [torch.from_numpy(h).cuda() for h in hs]
+    outs = pipeline._download(ds, torch)
+    for h, o in zip(hs, outs):
+        assert o.dtype == h.dtype and o.shape == h.shape
+        assert np.array_equal(o, h)
+        assert o.flags.writeable and o.flags.c_contiguous
