@@ -17,6 +17,18 @@ next to its sources), imports ``skewspmv`` from there and records:
   split_bands -> classify_conflicts -> spmv_serial / spmv_pars3).
 * ``hashes.json`` -- SHA-256 of every array of the same chain for c2 (and,
   with --big, c3 and c4, which take minutes and ~15 GB in the reference).
+* with --c5: the headline config c5 (n = 16.7 M, m = 216 M).  The COO route
+  (pattern_from_coo's np.unique over 2m keys, coo_normalize over 2m + n
+  triplets) needs ~25 min and ~70 GB here, so the chain is entered through
+  the reference's own validating constructors instead (``reference_chain_direct``):
+  ``AdjacencyPattern`` (reorder.py:34-63) over the symmetrised pattern,
+  the reference ``rcm_order`` (reorder.py:251-286), ``SssMatrix``
+  (formats.py:163-221) over the relabelled lower triangle, then the
+  reference ``split_bands`` / ``classify_conflicts`` / ``spmv_serial`` /
+  ``spmv_pars3``.  The two inputs that do not come from a reference
+  function -- the symmetrised pattern (oracle C restatement) and the
+  relabelled lower triangle (numpy restatement of apply_permutation +
+  coo_to_sss below) -- are exactly the stages the COO route pins on c2-c4.
 
 The inputs come from paper_2407_17651_b200.generators, so the GPU box
 (which has no /root/reference) regenerates identical inputs from seeds.
@@ -144,16 +156,104 @@ def reference_chain(R, cfg, ps=(1, 2, 4, 8)):
     return res
 
 
+def _relabel_lower(n, row_ptr, col_ind, off_diags, diags, forward):
+    """coo_to_sss(apply_permutation(coo, perm)) restated on the lower
+    triangle: entry (i, c, v) moves to (f[i], f[c]); when the relabel puts
+    it above the diagonal, its lower mirror (f[c], f[i]) carries -v
+    (formats.py:14-18 sign convention); rows sorted by (row, col) as
+    coo_normalize leaves them (formats.py:282-299)."""
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(row_ptr))
+    a = forward[rows]
+    b = forward[col_ind.astype(np.int64)]
+    del rows
+    swap = a < b
+    hi = np.where(swap, b, a)
+    lo = np.where(swap, a, b)
+    val = np.where(swap, -off_diags, off_diags)
+    del a, b, swap
+    key = hi * n + lo
+    del hi, lo
+    order = np.argsort(key, kind="stable")
+    key = key[order]
+    val = val[order]
+    del order
+    new_rows = key // n
+    col = key - new_rows * n
+    del key
+    counts = np.bincount(new_rows, minlength=n)
+    del new_rows
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=rp[1:])
+    dg = np.empty(n)
+    dg[forward] = diags
+    return rp, col, val, dg
+
+
+def reference_chain_direct(R, cfg, ps=(1, 2, 4, 8)):
+    """The reference chain entered through its validating constructors (see
+    the module docstring); returns the arrays to hash."""
+    from paper_2407_17651_b200 import generators as G
+    from oracle import oracle as O
+    g = G.make_config(cfg)
+    t = time.time()
+    ip, ix = O.pattern_from_sss(g.n, g.row_ptr, g.col_ind)
+    pat = R.AdjacencyPattern(g.n, ip, ix)  # reorder.py:34-63 validates
+    del ip, ix
+    perm = R.rcm_order(pat)
+    del pat
+    print(f"{cfg}: reference rcm_order {time.time() - t:.1f}s", flush=True)
+    rp, ci, od, dg = _relabel_lower(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags, perm.forward)
+    mode_alpha = float(g.diags[0]) if g.n else 0.0
+    del g
+    m = R.SssMatrix(len(rp) - 1, rp, ci, od, dg)  # formats.py:163-221 validates
+    del rp, ci, od, dg
+    assert np.all(m.diags == mode_alpha)
+    bw = R.compute_bandwidth(m)
+    beta = R.default_beta(m.n, bw)
+    x = G.make_x(m.n, G.CONFIGS[cfg]["seed_x"])
+    res = {"n": m.n, "nnz": m.nnz_offdiag, "bandwidth": bw, "beta": beta,
+           "rcm_forward": perm.forward, "row_ptr": m.row_ptr, "col_ind": m.col_ind,
+           "off_diags": m.off_diags, "diags": m.diags, "x": x}
+    y = R.spmv_serial(m, x)
+    res["y_serial"] = y
+    res["y_serial_norm_inf"] = float(np.max(np.abs(y)))
+    del y
+    print(f"{cfg}: relabel + serial {time.time() - t:.1f}s bw={bw} beta={beta}", flush=True)
+    for b, pp in ((beta, ps), (max(1, bw), (8,))):
+        s = R.split_bands(m, b)
+        for f in SPLIT_FIELDS:
+            res[f"b{b}/{f}"] = sha(getattr(s, f))
+        res[f"b{b}/middle_count"] = int(s.mid_col.size)
+        for p in pp:
+            plan, _ = R.classify_conflicts(s, R.partition_rows(m.n, p))
+            for f in PLAN_FIELDS:
+                res[f"b{b}/p{p}/{f}"] = sha(getattr(plan, f))
+            if p == 8:
+                res[f"b{b}/p{p}/y_pars3"] = sha(R.spmv_pars3(s, plan, x))
+            del plan
+        del s
+        print(f"{cfg}: beta={b} split/classify/pars3 {time.time() - t:.1f}s", flush=True)
+    return res
+
+
 def main():
     R = import_reference()
-    make_corpus(R)
-    c1 = reference_chain(R, "c1")
-    np.savez_compressed(os.path.join(HERE, "c1.npz"),
-                        **{k: np.asarray(v) for k, v in c1.items()})
     hashes = {}
     path = os.path.join(HERE, "hashes.json")
     if os.path.exists(path):
         hashes = json.load(open(path))
+    if "--c5" not in sys.argv:
+        make_corpus(R)
+        c1 = reference_chain(R, "c1")
+        np.savez_compressed(os.path.join(HERE, "c1.npz"),
+                            **{k: np.asarray(v) for k, v in c1.items()})
+    if "--c5" in sys.argv:  # only the headline config (see the module docstring)
+        res = reference_chain_direct(R, "c5")
+        hashes["c5"] = {k: (sha(v) if isinstance(v, np.ndarray) else v) for k, v in res.items()}
+        hashes["c5"]["route"] = "direct: AdjacencyPattern / rcm_order / SssMatrix / split_bands / classify_conflicts"
+        json.dump(hashes, open(path, "w"), indent=1, sort_keys=True)
+        print("hashes.json:", sorted(hashes))
+        return
     cfgs = ["c2"] + (["c3", "c4"] if "--big" in sys.argv else [])
     for cfg in cfgs:
         res = reference_chain(R, cfg)
