@@ -177,6 +177,17 @@ int pars3_dot(int64_t n, const double *a, const double *b, double *out, void *st
  * matrix VALUES already select fp64 accumulators at plan creation. */
 int pars3_plan_status(pars3_plan *plan, int32_t *flags, void *stream);
 
+/* The row-major plan a direct-mode product runs on (inspection / tests): the
+ * full CSR of A = D + L - L^T (lower entries, diagonal, negated mirrors per
+ * row, ascending columns) padded to warps of 512 entries; per lane of 16
+ * entries its first row and flags (bit k: entry k starts a row, bit 16: the
+ * entry after the lane starts one); the rows crossing warps with their first
+ * and last warp.  col == NULL: sizes[4] = {padded entries, entries, lanes,
+ * spanning rows} only. */
+int pars3_full_csr_host(const pars3_split_view *split, int64_t *sizes, int32_t *col, double *val,
+                        int32_t *lane_row, uint32_t *lane_flags, int32_t *span_row, int32_t *span_w0,
+                        int32_t *span_w1);
+
 /* Number of libpars3 kernels one pars3_plan_spmv (with_dot = 0) or
  * pars3_plan_spmv_dot (with_dot = 1) call launches (memsets excluded). */
 int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *count);

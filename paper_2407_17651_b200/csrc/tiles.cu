@@ -11,14 +11,30 @@
 //      into L2: lane l owns one row segment, keeps its row sum in registers
 //      (+a_ic * x_c, serial.py:56-57) and adds the mirror -a_ic * x_i
 //      (serial.py:58-59) into the tile's shared accumulator of column c --
-//      exact-integer fixed point with native 32-bit shared atomics (or fp64);
+//      exact-integer fixed point with native 32-bit shared atomics (or fp64
+//      for tiles the fixed point cannot carry: see the guard in tile_loop);
 //   3. every slot's accumulated value (+ diag * x for the tile's own rows)
-//      is reduced into y with fire-and-forget fp64 L2 reductions: for own
-//      rows this is the reference's owner write (parallel.py:85-95), for
-//      columns below the tile the accumulation message (msg_val /
-//      MPI_Accumulate, parallel.py:96-113).
-// y is zeroed on the stream first (pars3_plan_spmv) or accumulated into
-// (pars3_plan_spmv_acc).
+//      is delivered: for own rows this is the reference's owner write
+//      (parallel.py:85-95), for columns below the tile the accumulation
+//      message (msg_val / MPI_Accumulate, parallel.py:96-113).
+//
+// Delivery has two forms.
+//   GRID (single-GPU products, the default): every slot value is converted
+//      to an integer on one product-wide fixed-point grid and reduced into
+//      the int64 accumulator yacc with red.global.add.u64.  Integer sums
+//      commute, so the result does not depend on the order in which tiles
+//      arrive: the product is bitwise repeatable (the reference's own
+//      guarantee, parallel.py:107-108, tests/test_parallel.py:81-88).
+//      k_finish then streams yacc into fp64 y (clearing yacc for the next
+//      product) with the MRS dot <y, w> fused, summed in a fixed order.  The
+//      grid's scale needs a bound on |x|: the previous product's maximum (a
+//      pre-pass on the first product).  A product whose x exceeds it, holds
+//      a non-finite x, or whose grid turns out too coarse for its
+//      ||y||_inf, is redone by k_finish through the RED form (exact, IEEE).
+//   RED (peer mode, y += A x, the redo): fire-and-forget fp64
+//      red.global.add into y (zeroed first), or into a peer's inbox over
+//      NVLink.  Exact (the same per-tile guard), not bitwise repeatable.
+
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -30,6 +46,7 @@
 #include <new>
 
 #include "common.h"
+#include "fullcsr.h"
 #include "locality.h"
 #include "tileplan.h"
 
@@ -59,6 +76,7 @@ constexpr int kMaxWindowsDev = pars3::kMaxWindows;
 constexpr int kLocalExact = PARS3_CAP;  // window slots per tile: x + fp64 acc or two words (16 B/slot)
 constexpr int kLocalFixed = PARS3_CAP == 3200 ? 2496 : PARS3_CAP * 4 / 5 / 32 * 32;  // x + 3 words (20 B/slot)
 constexpr int kTerms2 = 64;        // two-word fixed point: max terms per slot per tile
+constexpr int kTerms3 = 4096;      // three-word fixed point: max terms per slot per tile
 // Shared arrays are laid out with a compile-time stride (so the second and
 // third accumulator words are an immediate offset from the first): the
 // plan's local space, then one spare slot and the SINK slot that padding
@@ -95,6 +113,29 @@ __device__ __forceinline__ int owner_of(const Peers &pr, int64_t g) {
     return r;
 }
 
+// Product state on the device (one per plan).  The kernels reset their own
+// counters, so a product needs no memset.
+struct GState {
+    int32_t claim;       // tile claims of the main pass (reset by k_finish)
+    int32_t claim2;      // tile claims of the redo pass (reset at its end)
+    int32_t flags;       // why the grid result must be redone (kFlag*), cleared by k_finish
+    int32_t xe;          // grid scale bound |x| < 2^xe assumed by the next product
+    int32_t xe_seen;     // max x exponent over this product's tiles
+    int32_t spare;
+    uint32_t bar;        // grid barrier of k_finish: arrivals
+    uint32_t gen;        // grid barrier of k_finish: generation
+    int32_t fp64_tiles;  // tiles accumulated in fp64 (guard or non-finite x), cumulative
+    int32_t redone;      // products redone by k_finish, cumulative
+    int32_t pad[6];
+};
+constexpr int kFlagNonfinite = 1;  // a non-finite x value: IEEE semantics need the fp64 form
+constexpr int kFlagXRange = 2;     // some |x| >= 2^xe: the grid could overflow
+constexpr int kFlagCoarse = 4;     // grid unit too coarse for this product's ||y||_inf
+constexpr int kFlagScale = 8;      // grid exponent outside the fp64 range
+constexpr int kFlagTileFp = 16;    // a tile the fixed point cannot carry (guard, scale range)
+constexpr int kXeNone = -1100;     // "no finite non-zero x seen"
+constexpr int kExNonfinite = 4000; // x exponent scan: a non-finite value
+
 struct DevPlan {
     const TileMeta *tiles;
     const Window *wins;
@@ -102,7 +143,6 @@ struct DevPlan {
     const uint8_t *rec;
     const int32_t *ucol;
     const double *diag;
-    int32_t *counter;
     int32_t ntiles;
     int32_t watchdog;
     int32_t diag_const;  // 1: every diagonal value equals diag_alpha (strict / shifted skew)
@@ -113,7 +153,17 @@ struct DevPlan {
                  // next tile's first slices at the end of the stream
     int32_t pf_dist;
     Peers peers;  // multi-GPU peer mode (nranks > 0): columns owned by other ranks
+    GState *gs;
+    // grid form: the int64 accumulator over the rows, per-CTA shares of the
+    // dot and of ||y||_inf (k_finish), the grid scale's bounds
+    long long *yacc;
+    double *blk_dot;
+    double *blk_max;
+    int32_t ev_g;   // every |value| and |diag| < 2^ev_g
+    int32_t hgrid;  // ceil(log2(most terms one y element sums))
+    int32_t cmax;   // most tiles delivering to one row block (grid roundings per element)
 };
+
 
 __device__ __forceinline__ uint32_t saddr(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -248,79 +298,189 @@ __device__ __forceinline__ void load_offsets(const DevPlan &P, const TileMeta &m
 }
 
 // ---- fixed-point accumulation ---------------------------------------------
-// A slot's mirror sum is kept as an exact integer Q * 2^(E-50) in three
-// 32-bit words (bits 0-19, 20-39, 40+ signed) updated with native
-// shared-memory integer adds (fire-and-forget ATOMS.ADD, no CAS loop).
-// E = ev + ex + 3 bounds every term of the tile (|v| < 2^ev, |x| < 2^ex,
-// a row segment sums <= 8 terms), so |Q| < 2^50 per term, each word takes up
-// to 4096 terms (a tile has <= 1024 rows), and the per-term rounding is
-// <= 2^(E-51).  Integer adds commute: a tile's accumulation is independent of
-// the order in which its warps arrive.
+// A slot's mirror sum is kept as an exact integer Q * 2^(E-50) in two (or
+// three) 32-bit words updated with native shared-memory integer adds
+// (fire-and-forget ATOMS.ADD, no CAS loop).  E = ev + ex + 3 bounds every
+// term of the tile (|v| < 2^ev, |x| < 2^ex, a row segment sums <= 8 terms),
+// so |Q| < 2^50 per term and the per-term rounding is <= 2^(E-51).  Integer
+// adds commute: a tile's accumulation is independent of the order in which
+// its warps arrive.
+//
+// q = fma(t, 2^(50-E), 1.5 * 2^52): the low mantissa bits hold rint(t *
+// 2^(50-E)) = Q as a two's-complement offset from the magic constant, so
+// the words come straight from the two halves of q.
+//   two words (<= kTerms2 = 64 terms per slot and tile, the plan checks):
+//     bits 0-25 unsigned (64 x 2^26 = 2^32), the signed rest Q >> 26;
+//   three words (<= 4096 terms): 20-bit limbs, the signed rest Q >> 40.
+//
+// Guard (the tile's accuracy is tied to its output, not to its bound E):
+// every row-segment sum (<= 8 terms, a partial output) also feeds qm =
+// max(Q >> 32) + 1024 and qn = OR of its bits.  A tile some of whose segment
+// sums are non-zero but none reaches |Q| >= 2^42 -- its bound E is more than
+// 8 bits above what it delivers, e.g. a large value met only by small x --
+// would round every term to a unit that is coarse against its output; it is
+// re-streamed with fp64 accumulators instead.  One
+// check per segment, not per term: 2-3 integer ops per lane and slice.
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-constexpr long long kMagicBits = 0x4338000000000000ll;
+constexpr uint32_t kGuardBig = 2048u;         // (Q >> 32) + 1024 >= 2048  <=>  |Q| >= 2^42
 
-__device__ __forceinline__ double fx_value(uint32_t lo, uint32_t mid, uint32_t hi, double unscale) {
-    const long long V = ((long long)(int32_t)hi << 40) + ((long long)mid << 20) + (long long)lo;
-    return (double)V * unscale;
-}
-
-// Two-word variant for tiles whose slots each take <= kTerms2 = 64 terms
-// (the plan checks): bits 0-25 in an unsigned word (64 x 2^26 = 2^32) and
-// the signed rest (|Q| < 2^50 -> |Q >> 26| < 2^24, 64 terms < 2^30).
-// q = fma(t, 2^(50-E), 1.5 * 2^52): the low mantissa bits hold rint(t * 2^(50-E))
-// = Q as a two's-complement offset from the magic constant, so the words
-// come straight from the two halves of q (bits 0-25, and Q >> 26).
-template <int kS>
-__device__ __forceinline__ void fx_add2m(uint32_t *w, uint32_t i, double q) {
+template <int kWords, int kS, bool kTrack = false>
+__device__ __forceinline__ void fx_add(uint32_t *w, uint32_t i, double q, uint32_t &qm, uint32_t &qn) {
     const uint32_t blo = (uint32_t)__double2loint(q);
     const uint32_t bhi = (uint32_t)__double2hiint(q) - 0x43380000u;  // Q >> 32
-    atomicAdd(w + i, blo & 0x3FFFFFFu);
-    atomicAdd(w + kS + i, __funnelshift_r(blo, bhi, 26));
+    if (kTrack) {
+        qm = max(qm, bhi + 1024u);
+        qn |= blo | bhi;
+    }
+    if (kWords == 3) {
+        atomicAdd(w + i, blo & 0xFFFFFu);
+        atomicAdd(w + kS + i, __funnelshift_r(blo, bhi, 20) & 0xFFFFFu);
+        atomicAdd(w + 2 * kS + i, (uint32_t)((int32_t)bhi >> 8));
+    } else {
+        atomicAdd(w + i, blo & 0x3FFFFFFu);
+        atomicAdd(w + kS + i, __funnelshift_r(blo, bhi, 26));
+    }
 }
 
-template <int kS>
-__device__ __forceinline__ void fx_add3m(uint32_t *w, uint32_t i, double q) {
-    const uint32_t blo = (uint32_t)__double2loint(q);
-    const uint32_t bhi = (uint32_t)__double2hiint(q) - 0x43380000u;
-    atomicAdd(w + i, blo & 0xFFFFFu);
-    atomicAdd(w + kS + i, __funnelshift_r(blo, bhi, 20) & 0xFFFFFu);
-    atomicAdd(w + 2 * kS + i, (uint32_t)((int32_t)bhi >> 8));
+// the exact integer Q of a slot (fixed point), clearing its words
+template <int kWords, int kS>
+__device__ __forceinline__ long long fx_take(uint32_t *w, int i) {
+    if (kWords == 3) {
+        const long long V = ((long long)(int32_t)w[2 * kS + i] << 40) + ((long long)w[kS + i] << 20) +
+                            (long long)w[i];
+        w[i] = w[kS + i] = w[2 * kS + i] = 0u;
+        return V;
+    }
+    const long long V = ((long long)(int32_t)w[kS + i] << 26) + (long long)w[i];
+    w[i] = w[kS + i] = 0u;
+    return V;
 }
 
-__device__ __forceinline__ double fx_value2(uint32_t lo, uint32_t hi, double unscale) {
-    const long long V = ((long long)(int32_t)hi << 26) + (long long)lo;
-    return (double)V * unscale;
+// Q * 2^sh on the grid, rounded half up when sh < 0 (deterministic)
+__device__ __forceinline__ long long to_grid(long long V, int sh) {
+    if (sh >= 0) return V << sh;  // sh <= 15 - hgrid: |result| < 2^62
+    if (sh < -62) return 0;
+    return (V + (1ll << (-sh - 1))) >> (-sh);
 }
 
-// kWords: 0 = fp64 shared accumulators (CAS loop per mirror), 2 / 3 =
-// exact-integer fixed point in two / three 32-bit words per slot.
-// kPeer: multi-GPU peer mode (P.peers); the single-GPU instantiation
-// compiles none of it.
-template <int kWords, bool kPeer>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
-k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
+__device__ __forceinline__ void red_add_u64(long long *p, long long v) {
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Stream a tile's slices into the shared accumulators.  kAcc: 2 / 3 fixed-
+// point words, 0 fp64 (shared atomicAdd, a CAS loop).
+template <int kAcc, int kS, uint32_t kSink>
+__device__ __forceinline__ void stream_tile(const DevPlan &P, const int64_t *off, int nsl, const double *xs,
+                                            uint32_t *wlo, double *acc, double scale, int warp, int lane,
+                                            uint32_t &qm, uint32_t &qn) {
+    for (int i = warp; i < nsl; i += kWarps) {
+        if ((P.pf & 2) && lane == 0 && i + P.pf_dist * kWarps < nsl) {
+            const int j = i + P.pf_dist * kWarps;
+            const int64_t a = off[j], b = off[j + 1];
+            bulk_prefetch_l2(P.rec + a * 16, (uint32_t)((b - a) * 16));
+        }
+        const uint8_t *rp = P.rec + off[i] * 16;
+        const int ns = (int)(((off[i + 1] - off[i]) * 16 - 64) / 320);
+        const uint32_t rl = __ldcs(reinterpret_cast<const uint16_t *>(rp) + lane);
+        const double *vp = reinterpret_cast<const double *>(rp + 64) + lane;
+        const uint16_t *ip = reinterpret_cast<const uint16_t *>(rp + 64 + ns * 256) + lane;
+        double v[kMaxSlots];
+        uint32_t li[kMaxSlots];
+#pragma unroll
+        for (int u = 0; u < kMaxSlots; u++) {
+            v[u] = 0.0;
+            li[u] = kSink;
+            if (u < ns) {  // warp-uniform; padding entries are (0, sink)
+                v[u] = __ldcs(vp + 32 * u);
+                li[u] = __ldcs(ip + 32 * u);
+            }
+        }
+        const double xr = xs[rl];
+        double c0 = 0.0, c1 = 0.0;  // two row-sum chains: even and odd slots
+        if (kAcc > 0) {
+            const double nxs = -xr * scale;  // mirror term v * (-x_r), scaled
+#pragma unroll
+            for (int u = 0; u < kMaxSlots; u++) {
+                if (u < ns) {
+                    if (u & 1)
+                        c1 = fma(v[u], xs[li[u]], c1);
+                    else
+                        c0 = fma(v[u], xs[li[u]], c0);
+                    fx_add<kAcc, kS>(wlo, li[u], fma(v[u], nxs, kMagic), qm, qn);
+                }
+            }
+            fx_add<kAcc, kS, true>(wlo, rl, fma(c0 + c1, scale, kMagic), qm, qn);
+        } else {
+#pragma unroll
+            for (int u = 0; u < kMaxSlots; u++) {
+                if (u < ns) {
+                    if (u & 1)
+                        c1 = fma(v[u], xs[li[u]], c1);
+                    else
+                        c0 = fma(v[u], xs[li[u]], c0);
+                    atomicAdd(&acc[li[u]], -v[u] * xr);
+                }
+            }
+            atomicAdd(&acc[rl], c0 + c1);
+        }
+    }
+}
+
+// Sum / max over the CTA with a fixed reduction tree (xor butterflies leave
+// the same value in every lane): deterministic.  Result valid in warp 0.
+__device__ __forceinline__ double cta_sum(double v, double *sred) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sred[warp] = v;
+    __syncthreads();
+    v = lane < kWarps ? sred[lane] : 0.0;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    return v;
+}
+__device__ __forceinline__ double cta_max(double v, double *sred) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) sred[warp] = v;
+    __syncthreads();
+    v = lane < kWarps ? sred[lane] : 0.0;
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    return v;
+}
+
+// The persistent tile loop.  kWords: the plan's accumulator (0 fp64, 2 / 3
+// fixed-point words; fixed-point plans switch single tiles to fp64).
+// kPeer: multi-GPU peer mode (P.peers; RED form only).  kGrid: GRID form
+// (y written by the block finalizers, w / dot: fused <y, w>, w == y when
+// dot_self) or RED form (fp64 reductions into y, zeroed by the caller).
+template <int kWords, bool kPeer, bool kGrid>
+__device__ __forceinline__ void tile_loop(const DevPlan &P, const double *__restrict__ x,
+                                          double *__restrict__ y, const double *w, double *dot,
+                                          bool dot_self, int32_t *claims) {
     constexpr bool kFixed = kWords > 0;
     constexpr int S = Layout<kWords>::kStride;
     constexpr uint32_t kSink = Layout<kWords>::kSink;
     extern __shared__ __align__(128) uint8_t dyn[];
     double *xs = reinterpret_cast<double *>(dyn);
-    // fp64 mode: acc[S]; fixed mode: two or three uint32 words per slot
+    // fp64 accumulators acc[S], or two / three uint32 words per slot (the
+    // fp64 view fits in either: a fixed-point plan's fp64 tiles use it)
     double *acc = xs + S;
     uint32_t *wlo = reinterpret_cast<uint32_t *>(xs + S);
-    uint32_t *wmid = wlo + S;  // two-word mode: the high word
-    uint32_t *whi = wmid + S;
     __shared__ int64_t s_off[2][kMaxTileSlices + 1];
     __shared__ int32_t s_t[3];  // tiles k, k+1 (known) and k+2 (claimed during tile k)
     __shared__ int32_t s_ex[2];
+    __shared__ uint32_t s_qm[2], s_qn[2];
     __shared__ __align__(8) uint64_t xbar;
     __shared__ TileCache s_tc[2];
+    __shared__ double s_red[kWarps];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int i = tid; i < S; i += kThreads) {
         xs[i] = 0.0;  // the sink's x stays 0
         if (kWords == 3) {
-            wlo[i] = wmid[i] = whi[i] = 0u;
+            wlo[i] = wlo[S + i] = wlo[2 * S + i] = 0u;
         } else if (kWords == 2) {
-            wlo[i] = wmid[i] = 0u;
+            wlo[i] = wlo[S + i] = 0u;
         } else {
             acc[i] = 0.0;
         }
@@ -328,13 +488,24 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
     // PARS3_PHASES=1: thread 0 accumulates SM cycles per phase
     // (totals in shared memory: no registers held across the tile loop)
     __shared__ long long s_clk[6];
-    if (tid < 6) s_clk[tid] = 0;
+    if (tid < 6) s_clk[tid] = 0;  // (phase 5: the grid form's arrivals, counted into slot 5)
+    // the grid of this product: yacc unit 2^(Eg-62), |partial sums| < 2^(Eg+1)
+    int Eg = 0, xe = 0;
+    if (kGrid) {
+        xe = *(volatile int32_t *)&P.gs->xe;
+        Eg = P.ev_g + xe + P.hgrid;
+        if (Eg > 960 || Eg < -960) {
+            if (tid == 0) atomicOr(&P.gs->flags, kFlagScale);
+            Eg = max(-960, min(960, Eg));
+        }
+    }
     if (tid == 0) {
         mbar_init(&xbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s_t[0] = atomicAdd(P.counter, 1);
-        s_t[1] = atomicAdd(P.counter, 1);
-        s_ex[0] = s_ex[1] = -1100;
+        s_t[0] = atomicAdd(claims, 1);
+        s_t[1] = atomicAdd(claims, 1);
+        s_ex[0] = s_ex[1] = kXeNone;
+        s_qm[0] = s_qm[1] = s_qn[0] = s_qn[1] = 0u;
         fetch_tile<kPeer>(P, s_t[0], s_tc[0]);
         issue_x_cached<kPeer>(P.peers, x, s_tc[0], xs, &xbar);
     }
@@ -359,7 +530,7 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
         const int nsl = tc.m.s1 - tc.m.s0;
         // claim tile k+2 now; the atomic's latency hides behind this tile
         int32_t claimed = 0;
-        if (tid == 0) claimed = atomicAdd(P.counter, 1);
+        if (tid == 0) claimed = atomicAdd(claims, 1);
         PHASE(0);
 
         // 1. x over the tile's local slots: windows arrived by TMA (issued
@@ -379,115 +550,85 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
                 }
             }
         } else {
-            for (int w = 0; w < tc.nw; w++) {
-                if (tma_ok<kPeer>(pr, x, tc, w)) continue;
-                const double *src = x + tc.lo[w];
+            for (int w2 = 0; w2 < tc.nw; w2++) {
+                if (tma_ok<kPeer>(pr, x, tc, w2)) continue;
+                const double *src = x + tc.lo[w2];
                 if (kPeer) {
-                    const int r = tc.own[w];
-                    if (r != pr.me) src = pr.x[r] + (pr.col_base + tc.lo[w] - pr.bs[r]);
+                    const int r = tc.own[w2];
+                    if (r != pr.me) src = pr.x[r] + (pr.col_base + tc.lo[w2] - pr.bs[r]);
                 }
-                for (int i = tid; i < tc.len[w]; i += kThreads) xs[tc.off[w] + i] = src[i];
+                for (int i = tid; i < tc.len[w2]; i += kThreads) xs[tc.off[w2] + i] = src[i];
             }
         }
         mbar_wait(&xbar, (uint32_t)(k & 1), P.watchdog, 5, t);
         asm volatile("cp.async.wait_all;" ::: "memory");  // this tile's record offsets
-        if (kFixed) {  // tile-wide bound on |x|: max binary exponent over the slots
-            // |x| < 2^(be - 1022) for normal x; slots in pairs (16-byte loads)
-            // (a subnormal x counts as exponent 1025: the tile is flagged below)
-            int e = -1100;
+        {  // tile-wide bound on |x|: max binary exponent over the slots, |x| < 2^ex
+            // (slots in pairs, 16-byte loads; a subnormal or zero x counts as
+            // 2^-1022; a non-finite one as kExNonfinite)
+            int e = kXeNone;
             const double2 *xs2 = reinterpret_cast<const double2 *>(xs);
             for (int i = tid; i < (local + 1) / 2; i += kThreads) {
                 const double2 v = xs2[i];  // (an odd tail's mate is inside the stride, not counted)
-                const long long q0 = __double_as_longlong(v.x), q1 = __double_as_longlong(v.y);
-                int b0 = (int)((q0 >> 52) & 0x7FF), b1 = (int)((q1 >> 52) & 0x7FF);
-                if (b0 == 0 && (q0 & 0xFFFFFFFFFFFFFll)) b0 = 2047;
-                if (b1 == 0 && (q1 & 0xFFFFFFFFFFFFFll)) b1 = 2047;
+                int b0 = (int)((__double_as_longlong(v.x) >> 52) & 0x7FF);
+                int b1 = (int)((__double_as_longlong(v.y) >> 52) & 0x7FF);
                 if (2 * i + 1 >= local) b1 = 0;
-                e = max(e, max(b0, b1) - 1022);
+                b0 = b0 == 2047 ? kExNonfinite : max(b0, 1) - 1022;
+                b1 = b1 == 2047 ? kExNonfinite : max(b1, 1) - 1022;
+                e = max(e, max(b0, b1));
             }
             e = __reduce_max_sync(0xffffffffu, e);
             if (lane == 0) atomicMax(&s_ex[cur], e);
         }
         __syncthreads();
         PHASE(1);
+        const int ex = s_ex[cur];
         if (tid == 0) {
             fetch_tile<kPeer>(P, s_t[(k + 1) % 3], s_tc[nxt]);  // overlaps the stream
-            s_ex[nxt] = -1100;
+            s_ex[nxt] = kXeNone;
+            s_qm[nxt] = s_qn[nxt] = 0u;
+            if (kGrid) {
+                if (ex >= kExNonfinite) {
+                    atomicOr(&P.gs->flags, kFlagNonfinite);
+                } else {
+                    if (ex > xe) atomicOr(&P.gs->flags, kFlagXRange);
+                    atomicMax(&P.gs->xe_seen, ex);  // (result unused: a fire-and-forget RED)
+                }
+            }
         }
-        int E = 0;
-        double scale = 0.0, unscale = 0.0;
-        if (kFixed) {
-            E = tc.m.ev + s_ex[cur] + 3;
-            // non-finite or subnormal x, or magnitudes the 2^(50-E) scale
-            // cannot carry: the tile's result is not exact -- raise the
-            // plan's status flag (the blocking entry points then redo the
-            // product with the fp64 kernel, pars3_plan_status)
-            if (tid == 0 && (E > 960 || (E < -960 && s_ex[cur] > -1022))) atomicOr(P.counter + 1, 1);
-            E = max(-960, min(960, E));
-            scale = ldexp(1.0, 50 - E);
-            unscale = ldexp(1.0, E - 50);
+        // the tile's fixed-point scale; fp64 accumulators for a non-finite x
+        // or a scale beyond the fp64 range (IEEE semantics).  The GRID form
+        // has no fp64 tile path (a leaner kernel): such a tile flags the
+        // product, which k_finish then redoes with fp64 accumulators.
+        constexpr bool kTileFp = kFixed && !kGrid;
+        int E = tc.m.ev + ex + 3;
+        bool tile_fp = !kFixed || ex >= kExNonfinite || E > 960;
+        if (kGrid && kFixed && tile_fp) {
+            if (tid == 0) atomicOr(&P.gs->flags, kFlagTileFp);
+            tile_fp = false;
         }
+        E = max(-960, min(960, E));
+        const double scale = ldexp(1.0, 50 - E);
+        const double unscale = ldexp(1.0, E - 50);
 
         // 2. records: each lane owns one row segment of a slice; row sums in
         //    registers, mirrors into the tile's shared accumulators
-        for (int i = warp; i < nsl; i += kWarps) {
-            if ((P.pf & 2) && lane == 0 && i + P.pf_dist * kWarps < nsl) {
-                const int j = i + P.pf_dist * kWarps;
-                const int64_t a = s_off[cur][j], b = s_off[cur][j + 1];
-                bulk_prefetch_l2(P.rec + a * 16, (uint32_t)((b - a) * 16));
-            }
-            const uint8_t *rp = P.rec + s_off[cur][i] * 16;
-            const int ns = (int)(((s_off[cur][i + 1] - s_off[cur][i]) * 16 - 64) / 320);
-            const uint32_t rl = __ldcs(reinterpret_cast<const uint16_t *>(rp) + lane);
-            const double *vp = reinterpret_cast<const double *>(rp + 64) + lane;
-            const uint16_t *ip = reinterpret_cast<const uint16_t *>(rp + 64 + ns * 256) + lane;
-            double v[kMaxSlots];
-            uint32_t li[kMaxSlots];
-#pragma unroll
-            for (int u = 0; u < kMaxSlots; u++) {
-                v[u] = 0.0;
-                li[u] = kSink;
-                if (u < ns) {  // warp-uniform; padding entries are (0, sink)
-                    v[u] = __ldcs(vp + 32 * u);
-                    li[u] = __ldcs(ip + 32 * u);
-                }
-            }
-            const double xr = xs[rl];
-            double c0 = 0.0, c1 = 0.0;  // two row-sum chains: even and odd slots
-            if (kFixed) {
-                const double nxs = -xr * scale;  // mirror term v * (-x_r), scaled
-#pragma unroll
-                for (int u = 0; u < kMaxSlots; u++) {
-                    if (u < ns) {
-                        if (u & 1)
-                            c1 = fma(v[u], xs[li[u]], c1);
-                        else
-                            c0 = fma(v[u], xs[li[u]], c0);
-                        const double q = fma(v[u], nxs, kMagic);
-                        if (kWords == 3)
-                            fx_add3m<S>(wlo, li[u], q);
-                        else
-                            fx_add2m<S>(wlo, li[u], q);
-                    }
-                }
-                const double q = fma(c0 + c1, scale, kMagic);
-                if (kWords == 3)
-                    fx_add3m<S>(wlo, rl, q);
-                else
-                    fx_add2m<S>(wlo, rl, q);
+        if constexpr (kFixed) {
+            if (kTileFp && tile_fp) {
+                uint32_t qm = 0, qn = 0;
+                stream_tile<0, S, kSink>(P, s_off[cur], nsl, xs, wlo, acc, 1.0, warp, lane, qm, qn);
             } else {
-#pragma unroll
-                for (int u = 0; u < kMaxSlots; u++) {
-                    if (u < ns) {
-                        if (u & 1)
-                            c1 = fma(v[u], xs[li[u]], c1);
-                        else
-                            c0 = fma(v[u], xs[li[u]], c0);
-                        atomicAdd(&acc[li[u]], -v[u] * xr);
-                    }
+                uint32_t qm = 0, qn = 0;
+                stream_tile<kWords, S, kSink>(P, s_off[cur], nsl, xs, wlo, acc, scale, warp, lane, qm, qn);
+                qm = __reduce_max_sync(0xffffffffu, qm);
+                qn = __reduce_or_sync(0xffffffffu, qn);
+                if (lane == 0 && (qm | qn)) {
+                    atomicMax(&s_qm[cur], qm);
+                    atomicOr(&s_qn[cur], qn);
                 }
-                atomicAdd(&acc[rl], c0 + c1);
             }
+        } else {
+            uint32_t qm = 0, qn = 0;
+            stream_tile<0, S, kSink>(P, s_off[cur], nsl, xs, wlo, acc, 1.0, warp, lane, qm, qn);
         }
         if (tid == 0) {
             s_t[(k + 2) % 3] = claimed;
@@ -501,6 +642,21 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
             }
         }
         __syncthreads();
+        if (kGrid && kFixed && s_qn[cur] != 0u && s_qm[cur] < kGuardBig) {
+            if (tid == 0) atomicOr(&P.gs->flags, kFlagTileFp);  // the guard: k_finish redoes
+        } else if (kTileFp && !tile_fp && s_qn[cur] != 0u && s_qm[cur] < kGuardBig) {
+            // the guard: re-stream this tile with fp64 accumulators
+            for (int i = tid; i < S; i += kThreads) {
+                acc[i] = 0.0;  // (words 0 .. 2S-1)
+                if (kWords == 3) wlo[2 * S + i] = 0u;
+            }
+            __syncthreads();
+            uint32_t qm = 0, qn = 0;
+            stream_tile<0, S, kSink>(P, s_off[cur], nsl, xs, wlo, acc, 1.0, warp, lane, qm, qn);
+            tile_fp = true;
+            __syncthreads();
+        }
+        if (kTileFp && tile_fp && tid == 0) atomicAdd(&P.gs->fp64_tiles, 1);
         PHASE(2);
 
         // 3. xs is free: the next tile's x windows and record offsets are
@@ -509,70 +665,88 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
         load_offsets(P, s_tc[nxt].m, s_off[nxt], tid);
         PHASE(4);
 
-        // 4. deliver: every slot's value (own rows + diag * x, x of own rows
-        //    from global: xs already holds the next tile) reduces into y with
-        //    a fire-and-forget fp64 red (consecutive slots -> coalesced L2
-        //    reductions); the accumulators are cleared in the same pass
-        auto take = [&](int i) -> double {
-            if (kWords == 3) {
-                const double a = fx_value(wlo[i], wmid[i], whi[i], unscale);
-                wlo[i] = wmid[i] = whi[i] = 0u;
-                return a;
-            }
-            if (kWords == 2) {
-                const double a = fx_value2(wlo[i], wmid[i], unscale);
-                wlo[i] = wmid[i] = 0u;
-                return a;
-            }
-            const double a = acc[i];
-            acc[i] = 0.0;
-            return a;
-        };
-        if (u0 >= 0) {
-            const int32_t *uc = P.ucol + u0;
-            const int nmsg = local - (r1 - r0);  // own rows are the tail of the list
-            for (int i = tid; i < local; i += kThreads) {
-                double a = take(i);
-                const int c = __ldg(uc + i);
-                double *dst = y + c;
-                bool mine = true;
-                if (kPeer) {  // a column of an earlier rank: its inbox, over NVLink
-                    const int64_t g = pr.col_base + c;
-                    const int r = owner_of(pr, g);
-                    if (r != pr.me) {
-                        dst = pr.y[r] + (g - pr.bs[r]);
-                        mine = false;
-                    }
+        // 4. deliver every slot (own rows: + diag * x, x of own rows from
+        //    global: xs already holds the next tile); the accumulators are
+        //    cleared in the same pass
+        if (kGrid) {
+            const double gscale = ldexp(1.0, 62 - Eg);
+            const int sh = E - Eg + 12;
+            auto deliver = [&](int i, int c) {
+                long long V;
+                if constexpr (kFixed) {
+                    V = to_grid(fx_take<kWords, S>(wlo, i), sh);
+                } else {
+                    V = __double2ll_rn(acc[i] * gscale);
+                    acc[i] = 0.0;
                 }
-                if (i >= nmsg && mine)  // (a halo row's diagonal belongs to its owner)
-                    a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), __ldg(x + c), a);
-                if (a != 0.0) atomicAdd(dst, a);
+                if (c >= r0 && c < r1)
+                    V += __double2ll_rn((P.diag_const ? P.diag_alpha : __ldg(P.diag + c)) * __ldg(x + c) *
+                                        gscale);
+                if (V != 0) red_add_u64(P.yacc + c, V);
+            };
+            if (u0 >= 0) {
+                const int32_t *uc = P.ucol + u0;
+                for (int i = tid; i < local; i += kThreads) deliver(i, __ldg(uc + i));
+            } else {
+                for (int w2 = 0; w2 < tc.nw; w2++)
+                    for (int i = tid; i < tc.len[w2]; i += kThreads) deliver(tc.off[w2] + i, tc.lo[w2] + i);
             }
+            __syncthreads();
+            PHASE(3);
         } else {
-            for (int w = 0; w < tc.nw; w++) {
-                const int lo = tc.lo[w], len = tc.len[w], off = tc.off[w];
-                // own columns reduce into y; an earlier rank's columns into its
-                // inbox over NVLink (peer mode; their diagonal is the owner's)
-                bool mine = true;
-                double *dst = y + lo;
-                if (kPeer) {
-                    const int r = tc.own[w];
-                    if (r != pr.me) {
-                        mine = false;
-                        dst = pr.y[r] + (pr.col_base + lo - pr.bs[r]);
+            auto take = [&](int i) -> double {
+                if constexpr (kFixed) {
+                    if (!(kTileFp && tile_fp)) return (double)fx_take<kWords, S>(wlo, i) * unscale;
+                }
+                const double a = acc[i];
+                acc[i] = 0.0;
+                return a;
+            };
+            if (u0 >= 0) {
+                const int32_t *uc = P.ucol + u0;
+                for (int i = tid; i < local; i += kThreads) {
+                    double a = take(i);
+                    const int c = __ldg(uc + i);
+                    double *dst = y + c;
+                    bool mine = true;
+                    if (kPeer) {  // a column of an earlier rank: its inbox, over NVLink
+                        const int64_t g = pr.col_base + c;
+                        const int r = owner_of(pr, g);
+                        if (r != pr.me) {
+                            dst = pr.y[r] + (g - pr.bs[r]);
+                            mine = false;
+                        }
+                    }
+                    if (mine && c >= r0 && c < r1)  // (a halo row's diagonal belongs to its owner)
+                        a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), __ldg(x + c), a);
+                    if (a != 0.0) atomicAdd(dst, a);
+                }
+            } else {
+                for (int w2 = 0; w2 < tc.nw; w2++) {
+                    const int lo = tc.lo[w2], len = tc.len[w2], off = tc.off[w2];
+                    // own columns reduce into y; an earlier rank's columns into its
+                    // inbox over NVLink (peer mode; their diagonal is the owner's)
+                    bool mine = true;
+                    double *dst = y + lo;
+                    if (kPeer) {
+                        const int r = tc.own[w2];
+                        if (r != pr.me) {
+                            mine = false;
+                            dst = pr.y[r] + (pr.col_base + lo - pr.bs[r]);
+                        }
+                    }
+                    for (int i = tid; i < len; i += kThreads) {
+                        const int c = lo + i;
+                        double a = take(off + i);
+                        if (mine && c >= r0 && c < r1)
+                            a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), __ldg(x + c), a);
+                        if (a != 0.0) atomicAdd(dst + i, a);
                     }
                 }
-                for (int i = tid; i < len; i += kThreads) {
-                    const int c = lo + i;
-                    double a = take(off + i);
-                    if (mine && c >= r0 && c < r1)
-                        a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), __ldg(x + c), a);
-                    if (a != 0.0) atomicAdd(dst + i, a);
-                }
             }
+            __syncthreads();
+            PHASE(3);
         }
-        __syncthreads();
-        PHASE(3);
     }
     // peer mode: this CTA's reductions into other GPUs' inboxes are performed
     // system-wide before the kernel completes (the barrier after the product
@@ -583,9 +757,184 @@ k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y) {
 #undef PHASE
 }
 
-// <a, b>: 16-byte loads, four in flight per thread, one fp64 atomic per block
+template <int kWords, bool kPeer, bool kGrid>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+k_tiles(DevPlan P, const double *__restrict__ x, double *__restrict__ y, const double *w, double *dot,
+        int dot_self) {
+    tile_loop<kWords, kPeer, kGrid>(P, x, y, w, dot, dot_self != 0, &P.gs->claim);
+}
+
+// grid barrier of k_finish (the kernel is launched cooperatively: every CTA
+// is resident)
+__device__ __forceinline__ void grid_sync(GState *g) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t gen = *(volatile uint32_t *)&g->gen;
+        __threadfence();
+        if (atomicAdd(&g->bar, 1u) == gridDim.x - 1) {
+            g->bar = 0u;
+            __threadfence();
+            atomicAdd(&g->gen, 1u);
+        } else {
+            while (*(volatile uint32_t *)&g->gen == gen) __nanosleep(256);  // (polls off the L2 path)
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// After every grid product (launched cooperatively: every CTA resident).
+// It first finishes the product in one streaming pass: y = yacc * 2^(Eg-62), yacc cleared, the
+// per-CTA shares of <y, w> and ||y||_inf (fixed row assignment), summed in
+// CTA order by CTA 0, which also runs the accuracy check and sets the next
+// scale bound.  Then, unless a kFlag* was raised (exits at once), the fp64
+// redo: y = 0, the RED form over every tile, <y, w> in a fixed order.
+// The redo accumulates in fp64 (shared-memory CAS, IEEE semantics for
+// non-finite and extreme inputs); the fp64 layout fits in every plan's
+// shared memory and its sink lies beyond every plan's local space.  Clears
+// the flags and resets the tile kernel's claim counter.
+constexpr int kFinishSmem = Layout<0>::kSmem;  // >= every plan's layout
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+k_finish(DevPlan P, const double *__restrict__ x, double *__restrict__ y, const double *w, double *dot,
+         int dot_self, int32_t n) {
+    GState *g = P.gs;
+    __shared__ double s_red[kWarps];
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    const int64_t i0 = blockIdx.x * (int64_t)kThreads + threadIdx.x;
+    {
+        const int xe = *(volatile int32_t *)&g->xe;
+        const int Eg = max(-960, min(960, P.ev_g + xe + P.hgrid));
+        const double gunit = ldexp(1.0, Eg - 62);
+        double d = 0.0, mx = 0.0;
+        const bool self = dot_self != 0;
+        if ((((uintptr_t)y | (uintptr_t)w) & 15) == 0) {  // pairs: 16-byte accesses
+            const int64_t n2 = n / 2;
+            longlong2 *a2 = reinterpret_cast<longlong2 *>(P.yacc);
+            double2 *y2 = reinterpret_cast<double2 *>(y);
+            const double2 *w2 = reinterpret_cast<const double2 *>(w);
+            for (int64_t i = i0; i < n2; i += 4 * stride) {  // four pairs in flight per thread
+                longlong2 Y[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (i + u * stride < n2) Y[u] = __ldcs(a2 + i + u * stride);
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int64_t j = i + u * stride;
+                    if (j < n2) {
+                        __stcs(a2 + j, make_longlong2(0, 0));
+                        const double2 v = make_double2((double)Y[u].x * gunit, (double)Y[u].y * gunit);
+                        __stcs(y2 + j, v);
+                        if (dot) {
+                            const double2 q = self ? v : __ldcs(w2 + j);
+                            d = fma(v.y, q.y, fma(v.x, q.x, d));
+                        }
+                        mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+                    }
+                }
+            }
+            if ((n & 1) && i0 == 0) {
+                const long long Y = P.yacc[n - 1];
+                P.yacc[n - 1] = 0;
+                const double v = (double)Y * gunit;
+                y[n - 1] = v;
+                if (dot) d = fma(v, self ? v : w[n - 1], d);
+                mx = fmax(mx, fabs(v));
+            }
+        } else {
+            for (int64_t i = i0; i < n; i += stride) {
+                const long long Y = P.yacc[i];
+                P.yacc[i] = 0;
+                const double v = (double)Y * gunit;
+                y[i] = v;
+                if (dot) d = fma(v, self ? v : w[i], d);
+                mx = fmax(mx, fabs(v));
+            }
+        }
+        d = cta_sum(d, s_red);
+        mx = cta_max(mx, s_red);
+        if (threadIdx.x == 0) {
+            P.blk_dot[blockIdx.x] = d;
+            P.blk_max[blockIdx.x] = mx;
+        }
+        grid_sync(g);
+        if (blockIdx.x == 0) {
+            d = 0.0;
+            mx = 0.0;
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) {
+                d += __ldcg(P.blk_dot + b);
+                mx = fmax(mx, __ldcg(P.blk_max + b));
+            }
+            d = cta_sum(d, s_red);
+            mx = cta_max(mx, s_red);
+            if (threadIdx.x == 0) {
+                if (dot) *dot = d;
+                // each delivery was rounded to the grid unit 2^(Eg-62) once:
+                // the grid's share of the error stays below 2^-44
+                // max(1, ||y||_inf), else the fp64 pass redoes the product
+                // (a matrix whose value range the x correlate with)
+                const double err = (double)P.cmax * ldexp(1.0, Eg - 63);
+                if (!(err <= ldexp(1.0, -44) * fmax(1.0, mx))) atomicOr(&g->flags, kFlagCoarse);
+                const int xs = *(volatile int32_t *)&g->xe_seen;
+                g->xe = (xs <= kXeNone ? -1000 : xs) + 1;
+                g->xe_seen = kXeNone;
+                __threadfence();
+            }
+        }
+        grid_sync(g);
+    }
+    if (__ldcg(&g->flags) == 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) g->claim = 0;
+        return;
+    }
+    for (int64_t i = i0; i < n; i += stride) y[i] = 0.0;
+    grid_sync(g);
+    tile_loop<0, false, false>(P, x, y, nullptr, nullptr, false, &g->claim2);  // fp64 accumulators
+    grid_sync(g);
+    if (dot) {  // per-CTA shares in blk_dot (>= kDotGrid entries), summed in CTA order
+        double d = 0.0;
+        for (int64_t i = i0; i < n; i += stride) {
+            const double v = __ldcg(y + i);
+            d = fma(v, dot_self ? v : w[i], d);
+        }
+        d = cta_sum(d, s_red);
+        if (threadIdx.x == 0) P.blk_dot[blockIdx.x] = d;
+    }
+    grid_sync(g);
+    if (blockIdx.x == 0) {
+        double d = 0.0;
+        if (dot)
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) d += __ldcg(P.blk_dot + b);
+        d = cta_sum(d, s_red);
+        if (threadIdx.x == 0) {
+            if (dot) *dot = d;
+            g->flags = 0;
+            g->claim = 0;
+            g->claim2 = 0;
+            g->redone++;
+            __threadfence();
+        }
+    }
+}
+
+// max binary exponent of x (|x| < 2^e) into gs->xe: the first grid product's
+// scale bound (later products use the previous one's maximum)
+__global__ void __launch_bounds__(512) k_xmax(int32_t n, const double *__restrict__ x, GState *g) {
+    int e = kXeNone;
+    const int32_t stride = gridDim.x * blockDim.x;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int b = (int)((__double_as_longlong(__ldcs(x + i)) >> 52) & 0x7FF);
+        if (b != 2047) e = max(e, max(b, 1) - 1022);
+    }
+    e = __reduce_max_sync(0xffffffffu, e);
+    if ((threadIdx.x & 31) == 0 && e > kXeNone) atomicMax(&g->xe, e + 1);
+}
+
+// <a, b>: 16-byte loads, four in flight per thread; each block writes its
+// share to part[blockIdx.x] and k_sum_parts adds the shares in block order
+// (a fixed reduction order: the dot is bitwise repeatable)
+constexpr int kDotGrid = 148 * 4;
 __global__ void __launch_bounds__(512) k_dot(int32_t n, const double *__restrict__ a,
-                                             const double *__restrict__ b, double *out) {
+                                             const double *__restrict__ b, double *part) {
     double s = 0.0;
     const int64_t n2 = n / 2;
     const double2 *a2 = reinterpret_cast<const double2 *>(a);
@@ -614,8 +963,18 @@ __global__ void __launch_bounds__(512) k_dot(int32_t n, const double *__restrict
     if (threadIdx.x < 32) {
         s = threadIdx.x < 16 ? ws[threadIdx.x] : 0.0;
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (threadIdx.x == 0) atomicAdd(out, s);
+        if (threadIdx.x == 0) part[blockIdx.x] = s;
     }
+}
+
+// *out = sum of part[0 .. np) in index order (one CTA, fixed tree)
+__global__ void __launch_bounds__(kThreads) k_sum_parts(int32_t np, const double *__restrict__ part,
+                                                        double *out) {
+    __shared__ double s_red[kWarps];
+    double d = 0.0;
+    for (int i = threadIdx.x; i < np; i += kThreads) d += part[i];
+    d = cta_sum(d, s_red);
+    if (threadIdx.x == 0) *out = d;
 }
 
 // locality order (locality.cpp): xs[j] = x[inv[j]] (gather: the random
@@ -638,7 +997,8 @@ __global__ void __launch_bounds__(512) k_perm_in(int32_t n, const int32_t *__res
     for (; j < n; j += stride) __stcs(xs + j, __ldg(x + __ldcs(inv + j)));
 }
 
-// y[i] = (acc ? y[i] : 0) + ys[perm[i]]; with dot: *dot += <y, w> (w == y allowed)
+// y[i] = (acc ? y[i] : 0) + ys[perm[i]]; with dot: part[blockIdx.x] = this
+// block's share of <y, w> (w == y allowed; k_sum_parts adds them in order)
 template <bool kAcc, bool kDot>
 __global__ void __launch_bounds__(512) k_perm_out(int32_t n, const int32_t *__restrict__ perm,
                                                   const double *__restrict__ ys, double *y,
@@ -675,84 +1035,132 @@ __global__ void __launch_bounds__(512) k_perm_out(int32_t n, const int32_t *__re
     if (threadIdx.x < 32) {
         s = threadIdx.x < 16 ? ws[threadIdx.x] : 0.0;
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (threadIdx.x == 0) atomicAdd(dot, s);
+        if (threadIdx.x == 0) dot[blockIdx.x] = s;
     }
 }
 
-// Direct mode (plans whose tiles would hold about one entry per shared
-// slot, e.g. c4's R-MAT): no shared staging.  y = d.x (+ y) first, then
-// every stored entry a_rc gathers x_c into its row's register sum and
-// reduces -a_rc x_r straight into y_c (fp64 red.global.add, L2).  Each lane
-// owns kDirectRun consecutive entries (row-major) and issues all their x
-// gathers at once, so long rows spread over lanes and warps (nnz-balanced),
-// and a lane reduces its row sum once per row run.
-
-__global__ void __launch_bounds__(512) k_direct_init(int32_t n, const double *__restrict__ diag,
-                                                     double alpha, const double *__restrict__ x,
-                                                     double *y, int acc) {
-    const int32_t stride = gridDim.x * blockDim.x;
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const double d = diag ? diag[i] : alpha;
-        const double v = d * __ldg(x + i);
-        y[i] = acc ? y[i] + v : v;
-    }
-}
-
-template <int kDirectRun>
-__global__ void __launch_bounds__(256) k_direct(int64_t m, const int32_t *__restrict__ row,
-                                                const int32_t *__restrict__ col,
+// Row-major form (plans whose tiles would stage about one entry per shared
+// slot, e.g. c4's R-MAT, or would leave the grid idle, c2): the full CSR of
+// A = D + L - L^T (fullcsr.h).  Each lane owns 16 consecutive entries: it
+// issues their 16 x gathers at once and sums its row segments in order.  A
+// row complete inside a lane is written by that lane; a row crossing lanes
+// is summed by a fixed-order warp scan of the lanes' partials (the operator
+// (m, t) o (m', t') = (m m', t + m t') over "the lane holds no row start");
+// a row crossing warps is summed by k_csr_fix from the warps' tail / head
+// partials in warp order.  No atomics: every y element is written once, the
+// sum order is fixed by the plan (bitwise repeatable), and the arithmetic
+// is plain fp64 (IEEE semantics for non-finite inputs).
+__global__ void __launch_bounds__(256, 2) k_csr(int64_t ne, int64_t nwarps, const int32_t *__restrict__ col,
                                                 const double *__restrict__ val,
-                                                const double *__restrict__ x, double *y) {
-    const int64_t nrun = (m + kDirectRun - 1) / kDirectRun;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nrun; t += stride) {
-        const int64_t e0 = t * kDirectRun;
-        int32_t r[kDirectRun], c[kDirectRun];
-        double v[kDirectRun];
-        if (e0 + kDirectRun <= m) {  // 16-byte loads (the arrays are 16-byte aligned, runs of 8)
-            const int4 *r4 = reinterpret_cast<const int4 *>(row + e0);
-            const int4 *c4 = reinterpret_cast<const int4 *>(col + e0);
-            const double2 *v2 = reinterpret_cast<const double2 *>(val + e0);
+                                                const int32_t *__restrict__ lane_row,
+                                                const uint32_t *__restrict__ lane_flags,
+                                                const double *__restrict__ x, double *__restrict__ y,
+                                                double *__restrict__ whead, double *__restrict__ wtail) {
+    constexpr int K = pars3::kCsrLane;
+    const int lane = threadIdx.x & 31;
+    const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < nwarps; w += wstride) {
+        const int64_t L = w * 32 + lane, e0 = L * K;
+        int32_t c[K];
+        double v[K], xc[K];
+        const int4 *c4 = reinterpret_cast<const int4 *>(col + e0);
+        const double2 *v2 = reinterpret_cast<const double2 *>(val + e0);
 #pragma unroll
-            for (int h = 0; h < kDirectRun / 4; h++) {
-                const int4 a = __ldcs(r4 + h), b = __ldcs(c4 + h);
-                r[4 * h] = a.x; r[4 * h + 1] = a.y; r[4 * h + 2] = a.z; r[4 * h + 3] = a.w;
-                c[4 * h] = b.x; c[4 * h + 1] = b.y; c[4 * h + 2] = b.z; c[4 * h + 3] = b.w;
+        for (int h = 0; h < K / 4; h++) {
+            const int4 a = __ldcs(c4 + h);
+            c[4 * h] = a.x;
+            c[4 * h + 1] = a.y;
+            c[4 * h + 2] = a.z;
+            c[4 * h + 3] = a.w;
+        }
+        const int32_t row0 = __ldcs(lane_row + L);
+        const uint32_t fl = __ldcs(lane_flags + L);
+#pragma unroll
+        for (int k = 0; k < K; k++) xc[k] = e0 + k < ne ? __ldg(x + c[k]) : 0.0;  // all in flight
+#pragma unroll
+        for (int h = 0; h < K / 2; h++) {
+            const double2 a = __ldcs(v2 + h);
+            v[2 * h] = a.x;
+            v[2 * h + 1] = a.y;
+        }
+        // the lane's row segments, in order
+        const bool cont = !(fl & 1u);  // the first entry continues a row of an earlier lane
+        bool first = true;
+        double head = 0.0, s = 0.0;
+        int32_t r = row0;
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            if (k > 0 && ((fl >> k) & 1u)) {
+                if (first && cont)
+                    head = s;
+                else
+                    y[r] = s;
+                first = false;
+                r++;
+                s = 0.0;
             }
+            s = fma(v[k], xc[k], s);
+        }
+        const bool open = !((fl >> K) & 1u);
+        if (!open) {
+            if (first && cont)
+                head = s;
+            else
+                y[r] = s;
+        }
+        const bool single = first && cont && open;
+        // fixed-order warp scan: out_l = t_l + m_l * out_{l-1}
+        double t = open ? s : 0.0;
+        int m = single ? 1 : 0;
 #pragma unroll
-            for (int h = 0; h < kDirectRun / 2; h++) {
-                const double2 a = __ldcs(v2 + h);
-                v[2 * h] = a.x;
-                v[2 * h + 1] = a.y;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < kDirectRun; j++) {
-                const bool in = e0 + j < m;
-                r[j] = in ? row[e0 + j] : (j ? r[j - 1] : 0);
-                c[j] = in ? col[e0 + j] : -1;  // -1: past the end
-                v[j] = in ? val[e0 + j] : 0.0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double tp = __shfl_up_sync(0xffffffffu, t, o);
+            const int mp = __shfl_up_sync(0xffffffffu, m, o);
+            if (lane >= o) {
+                if (m) t = t + tp;
+                m &= mp;
             }
         }
-        double xc[kDirectRun];
-#pragma unroll
-        for (int j = 0; j < kDirectRun; j++) xc[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;  // all in flight
-        int32_t cur = r[0];
-        double xr = __ldg(x + cur), acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < kDirectRun; j++) {
-            if (r[j] != cur) {
-                atomicAdd(y + cur, acc);
-                cur = r[j];
-                xr = __ldg(x + cur);
-                acc = 0.0;
-            }
-            if (c[j] < 0) break;
-            acc = fma(v[j], xc[j], acc);
-            atomicAdd(y + c[j], -v[j] * xr);
+        // (every lane takes part in the shuffles)
+        const double tin = __shfl_up_sync(0xffffffffu, t, 1);
+        const int mup = __shfl_up_sync(0xffffffffu, m, 1);
+        const double in = lane == 0 ? 0.0 : tin;
+        const int reach = lane == 0 ? 1 : mup;  // the lanes before are all single
+        if (cont && !single) {  // this lane closes a row continued from earlier lanes
+            const double a = head + in;
+            if (reach)
+                whead[w] = a;  // the row started in an earlier warp: k_csr_fix completes it
+            else
+                y[row0] = a;
         }
-        atomicAdd(y + cur, acc);
+        if (lane == 31 && open) {
+            if (m)
+                whead[w] = t;  // the whole warp lies inside one row
+            else
+                wtail[w] = t;  // the last row's partial: it started in this warp
+        }
     }
+}
+
+// rows crossing warps: y[row] = tail[w0] + head[w0 + 1] + ... + head[w1]
+__global__ void __launch_bounds__(256) k_csr_fix(int32_t nspan, const int32_t *__restrict__ row,
+                                                 const int32_t *__restrict__ w0, const int32_t *__restrict__ w1,
+                                                 const double *__restrict__ whead,
+                                                 const double *__restrict__ wtail, double *__restrict__ y) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nspan) return;
+    const int32_t a = w0[i], b = w1[i];
+    double s = wtail[a];
+    int32_t w = a + 1;
+    for (; w + 3 <= b; w += 4) {  // four loads in flight, summed in order
+        const double h0 = whead[w], h1 = whead[w + 1], h2 = whead[w + 2], h3 = whead[w + 3];
+        s = s + h0;
+        s = s + h1;
+        s = s + h2;
+        s = s + h3;
+    }
+    for (; w <= b; w++) s = s + whead[w];
+    y[row[i]] = s;
 }
 
 template <class T>
@@ -764,6 +1172,7 @@ int upload(T **dst, const std::vector<T> &src) {
     return PARS3_OK;
 }
 
+
 }  // namespace
 
 struct pars3_plan {
@@ -771,7 +1180,7 @@ struct pars3_plan {
     int32_t p = 1;
     int32_t ntiles = 0, nslices = 0, lmax = 0;
     int64_t nnz = 0, slots = 0, nwins = 0;
-    int grid = 0;
+    int grid = 0, grid_redo = 0;
     size_t smem = 0;
     TileMeta *tiles = nullptr;
     Window *wins = nullptr;
@@ -782,24 +1191,30 @@ struct pars3_plan {
     int32_t list_tiles = 0, watchdog = 0, diag_const = 0, words = 0, pf = 0, pf_dist = 1;
     double diag_alpha = 0.0;
     unsigned long long *phase_clk = nullptr;
-    int32_t *counter = nullptr;
+    GState *gs = nullptr;
     int64_t bytes = 0;
     Peers peers{};
+    // grid form (deterministic single-GPU products)
+    int32_t grid_ok = 0, xe_ready = 0, ev_g = 0, hgrid = 0, cmax = 0;
+    double *blk_dot = nullptr, *blk_max = nullptr, *part = nullptr;
+    long long *yacc = nullptr;
+    int32_t seen_fp64_tiles = 0, seen_redone = 0;  // pars3_plan_status: counters at its last call
     // internal locality order (locality.cpp): the tiles hold P A P^T, x and
     // y pass through perm (split label -> internal label) and xs / ys
     int32_t *perm = nullptr, *iperm = nullptr;
     double *xs = nullptr, *ys = nullptr;
     int64_t local_slots = 0, dropped = 0;
-    // direct mode (k_direct): row-major entries, no tiles
-    int32_t direct = 0, direct_run = 16;  // entries per lane: 16 measured best on c4 (4: 1.00 ms,
-                                          // 8: 0.89, 16: 0.83; profiles/r01/sweep_direct_run_c4.txt)
-    int64_t dm = 0;
-    int32_t *drow = nullptr, *dcol = nullptr;
-    double *dval = nullptr;
+    // row-major form (k_csr): the full CSR of A in lanes of 16 entries, no tiles
+    int32_t direct = 0, nspan = 0;
+    int64_t ne = 0, nwarps = 0;
+    int32_t *ccol = nullptr, *clrow = nullptr, *span_row = nullptr, *span_w0 = nullptr, *span_w1 = nullptr;
+    uint32_t *clflags = nullptr;
+    double *cval = nullptr, *whead = nullptr, *wtail = nullptr, *yacc_tmp = nullptr;
 
     ~pars3_plan() {
-        void *ptrs[] = {tiles, wins, slice_off, rec, ucol, diag, counter, phase_clk, perm, iperm, xs, ys,
-                        drow, dcol, dval};
+        void *ptrs[] = {tiles, wins, slice_off, rec,    ucol,    diag, gs,   phase_clk, perm,
+                        iperm, xs,   ys,        ccol,   cval,    clrow, clflags, span_row, span_w0,
+                        span_w1, whead, wtail, yacc_tmp, blk_dot, blk_max, part, yacc};
         for (void *q : ptrs)
             if (q) cudaFree(q);
     }
@@ -818,7 +1233,81 @@ static bool values_fixed_point_safe(const pars3_split_view *s) {
     };
     if (nm > 0) check(s->mid_val, nm);
     if (s->outer_count > 0) check(s->outer_val, s->outer_count);
+    if (s->n > 0) check(s->diag, s->n);
     return ok;
+}
+
+// The grid form's bounds: the most tiles delivering to one row block (each
+// delivery is one rounding to the grid), the most terms one y element sums
+// (Dmax: its row's entries, its column's mirrors and its diagonal: the
+// grid's headroom) and the largest value exponent.  Every row must belong
+// to a tile (no SKIP_EMPTY).
+struct GridData {
+    int32_t hgrid = 0, cmax = 0, ev_g = -1074;
+};
+
+static int grid_data(const pars3_split_view *v, const HostPlan &hp, GridData &G) {
+    const int64_t n = v->n;
+    const int64_t nt = (int64_t)hp.tiles.size();
+    std::vector<int32_t> blk(n, -1);
+    for (int64_t t = 0; t < nt; t++)
+        for (int32_t r = hp.tiles[t].r0; r < hp.tiles[t].r1; r++) blk[r] = (int32_t)t;
+    for (int64_t r = 0; r < n; r++)
+        if (blk[r] < 0) PARS3_FAIL(PARS3_ERR_STRUCT, "grid form: row %lld belongs to no tile", (long long)r);
+    std::vector<std::vector<int32_t>> lists(nt);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t t = 0; t < nt; t++) {
+        const TileMeta &m = hp.tiles[t];
+        std::vector<int32_t> &L = lists[t];
+        if (m.u0 >= 0) {
+            int32_t last = -1;
+            for (int32_t i = 0; i < m.local; i++) {
+                const int32_t b = blk[hp.ucol[m.u0 + i]];
+                if (b != last) L.push_back(last = b);
+            }
+        } else {
+            for (int32_t w = m.w0; w < m.w1; w++) {
+                int64_t c = hp.wins[w].lo;
+                const int64_t hi = c + hp.wins[w].len;
+                while (c < hi) {
+                    const int32_t b = blk[c];
+                    L.push_back(b);
+                    c = hp.tiles[b].r1;
+                }
+            }
+        }
+        std::sort(L.begin(), L.end());
+        L.erase(std::unique(L.begin(), L.end()), L.end());
+    }
+    std::vector<int32_t> need(nt, 0);  // tiles delivering to each row block
+    for (int64_t t = 0; t < nt; t++)
+        for (int32_t b : lists[t]) need[b]++;
+    for (int64_t t = 0; t < nt; t++) {
+        G.cmax = std::max(G.cmax, need[t]);
+        G.ev_g = std::max(G.ev_g, hp.tiles[t].ev);
+    }
+    // terms per y element: row entries + column mirrors + the diagonal
+    std::vector<int32_t> terms(n, 1);
+    const int64_t nm = v->mid_ptr ? v->mid_ptr[n] : 0;
+    for (int64_t r = 0; r < n; r++) terms[r] += (int32_t)(v->mid_ptr[r + 1] - v->mid_ptr[r]);
+    for (int64_t k = 0; k < nm; k++) terms[v->mid_col[k]]++;
+    for (int64_t k = 0; k < v->outer_count; k++) {
+        terms[v->outer_row[k]]++;
+        terms[v->outer_col[k]]++;
+    }
+    int64_t dmax = 1;
+    double dg = 0.0;
+    for (int64_t r = 0; r < n; r++) {
+        dmax = std::max<int64_t>(dmax, terms[r]);
+        dg = std::max(dg, std::fabs(v->diag[r]));
+    }
+    while ((1ll << G.hgrid) < dmax) G.hgrid++;
+    if (dg > 0.0) {
+        int e = 0;
+        std::frexp(dg, &e);  // |diag| < 2^e
+        G.ev_g = std::max(G.ev_g, e);
+    }
+    return PARS3_OK;
 }
 
 extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_options *opt,
@@ -847,11 +1336,12 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     // accumulation of the mirror sums: mode 2 = fp64 shared accumulators,
     // mode 1 = exact-integer fixed point in three words, mode 3 = two words
     // (needs <= kTerms2 terms per slot and tile), mode 0 = auto: two words
-    // when the plan allows, else fp64 for window-structured matrices and
-    // three words when most tiles are unstructured list tiles
+    // when the plan allows, else three words (<= 4096 terms; exact integer
+    // sums keep the product bitwise repeatable), else fp64
     const int req_mode = opt ? opt->mode : 0;
+    const bool safe_values = values_fixed_point_safe(s);
     int words0 = req_mode == 1 ? 3 : req_mode == 2 ? 0 : 2;
-    if (words0 && !values_fixed_point_safe(s)) words0 = 0;  // fp64 accumulators keep IEEE semantics
+    if (words0 && !safe_values) words0 = 0;  // fp64 accumulators keep IEEE semantics
     // the shared-memory budget (x + accumulators per slot, 4 CTAs / SM) caps both
     if (o0.seg_max > 8) o0.seg_max = 8;
     const int32_t want_local = o0.local_slots;
@@ -870,17 +1360,21 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
             if (req_mode == 3)
                 PARS3_FAIL(PARS3_ERR_ARG, "two-word accumulation needs <= %d terms per slot, plan has %d",
                            kTerms2, hp.max_terms);
+            words = 3;
+            o.terms_cap = 0;
+            o.local_slots = std::min(want_local, kLocalFixed);
+            o.sink = (uint16_t)Layout<3>::kSink;
+            hp = HostPlan();
+            rc = pars3::build_tile_plan(v->n, v->mid_ptr, v->mid_col, v->mid_val, v->outer_count,
+                                        v->outer_row, v->outer_col, v->outer_val, o, hp);
+            if (rc) return rc;
+        }
+        // the three 20-bit limbs carry <= 4096 terms per slot and tile
+        if (words == 3 && hp.max_terms > kTerms3) {
+            if (req_mode == 1)
+                PARS3_FAIL(PARS3_ERR_ARG, "three-word accumulation needs <= %d terms per slot, plan has %d",
+                           kTerms3, hp.max_terms);
             words = 0;
-            if (4ll * hp.list_tiles > (int64_t)hp.tiles.size()) {
-                words = 3;
-                o.terms_cap = 0;
-                o.local_slots = std::min(want_local, kLocalFixed);
-                o.sink = (uint16_t)Layout<3>::kSink;
-                hp = HostPlan();
-                rc = pars3::build_tile_plan(v->n, v->mid_ptr, v->mid_col, v->mid_val, v->outer_count,
-                                            v->outer_row, v->outer_col, v->outer_val, o, hp);
-                if (rc) return rc;
-            }
         }
         return PARS3_OK;
     };
@@ -922,6 +1416,11 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
             lo = LocalityOrder();
         }
     }
+    // the split the tiles were built from (the caller's, or P A P^T)
+    pars3_split_view used = *s;
+    if (!lo.forward.empty())
+        used = pars3_split_view{s->n, s->beta, lo.diag.data(), lo.row_ptr.data(), lo.col.data(),
+                                lo.val.data(), 0, nullptr, nullptr, nullptr};
     // direct mode: the tiles would stage about one entry per slot (no reuse
     // of x or of the accumulators in shared memory), or a mid-size matrix
     // whose tiles would leave most of the persistent grid idle (c2: 256
@@ -938,33 +1437,25 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_SKIP_EMPTY | PARS3_PLAN_NO_DIRECT)) &&
         ((flags & PARS3_PLAN_DIRECT) || few_tiles ||
          (2ll * hp.list_tiles > (int64_t)hp.tiles.size() && 10 * local >= 9 * hp.nnz));
-    std::vector<int32_t> drow, dcol;
-    std::vector<double> dval;
-    if (direct) {  // row-major entries: a row's outer entries, then its middle ones
+    pars3::FullCsr F;
+    if (direct) {  // the full CSR of A (fullcsr.cpp)
+        rc = pars3::build_full_csr(s, F);
+        if (rc) return rc;
+        const int64_t m_entries = hp.nnz;
+        hp = HostPlan();  // no tiles are uploaded
+        hp.nnz = m_entries;
+    }
+    // grid form: single-GPU tile plans over finite, fixed-point-safe values
+    // where every row belongs to a tile
+    GridData G;
+    const bool grid_ok = !direct && !hp.tiles.empty() && safe_values && !o0.skip_empty;
+    if (grid_ok) {
         try {
-            const int64_t m = (s->mid_ptr ? s->mid_ptr[s->n] : 0) + s->outer_count;
-            drow.resize(m);
-            dcol.resize(m);
-            dval.resize(m);
-            int64_t o_k = 0, e = 0;
-            for (int64_t i = 0; i < s->n; i++) {
-                for (; o_k < s->outer_count && s->outer_row[o_k] == i; o_k++, e++) {
-                    drow[e] = (int32_t)i;
-                    dcol[e] = s->outer_col[o_k];
-                    dval[e] = s->outer_val[o_k];
-                }
-                for (int64_t k = s->mid_ptr[i]; k < s->mid_ptr[i + 1]; k++, e++) {
-                    drow[e] = (int32_t)i;
-                    dcol[e] = s->mid_col[k];
-                    dval[e] = s->mid_val[k];
-                }
-            }
-            if (e != m) PARS3_FAIL(PARS3_ERR_STRUCT, "outer rows are not sorted");
+            rc = grid_data(&used, hp, G);
         } catch (const std::bad_alloc &) {
             PARS3_FAIL(PARS3_ERR_NOMEM, "out of host memory");
         }
-        hp = HostPlan();  // no tiles are uploaded
-        hp.nnz = (int64_t)dval.size();
+        if (rc) return rc;
     }
     pars3_plan *pl = new (std::nothrow) pars3_plan;
     if (!pl) PARS3_FAIL(PARS3_ERR_NOMEM, "out of host memory");
@@ -991,6 +1482,8 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
             cudaMalloc((void **)&pl->phase_clk, 8 * sizeof(unsigned long long));
             cudaMemset(pl->phase_clk, 0, 8 * sizeof(unsigned long long));
         }
+        const char *ng = getenv("PARS3_NO_GRID");  // A/B knob: the RED form for every product
+        pl->grid_ok = grid_ok && !(ng && ng[0] == '1');
     }
     pl->local_slots = local;
     pl->dropped = lo.dropped;
@@ -1009,14 +1502,29 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         }                                          \
         pl->bytes += sizeof(src[0]) * src.size();  \
     } while (0)
+#define ZALLOC(dst, count)                                                                    \
+    do {                                                                                      \
+        const size_t _b = sizeof(*pl->dst) * (size_t)(count);                                 \
+        if (cudaMalloc((void **)&pl->dst, _b) != cudaSuccess || cudaMemset(pl->dst, 0, _b) != cudaSuccess) { \
+            delete pl;                                                                        \
+            PARS3_FAIL(PARS3_ERR_CUDA, "cudaMalloc failed");                                  \
+        }                                                                                     \
+        pl->bytes += (int64_t)_b;                                                             \
+    } while (0)
     if (direct) {
         pl->direct = 1;
-        if (const char *dr = getenv("PARS3_DIRECT_RUN")) pl->direct_run = atoi(dr);  // tuning knob
-        if (pl->direct_run != 4 && pl->direct_run != 8) pl->direct_run = 16;
-        pl->dm = (int64_t)dval.size();
-        UP(drow, drow);
-        UP(dcol, dcol);
-        UP(dval, dval);
+        pl->ne = F.ne;
+        pl->nwarps = (int64_t)F.col.size() / pars3::kCsrWarp;
+        pl->nspan = (int32_t)F.span_row.size();
+        UP(ccol, F.col);
+        UP(cval, F.val);
+        UP(clrow, F.lane_row);
+        UP(clflags, F.lane_flags);
+        UP(span_row, F.span_row);
+        UP(span_w0, F.span_w0);
+        UP(span_w1, F.span_w1);
+        ZALLOC(whead, std::max<int64_t>(1, pl->nwarps));
+        ZALLOC(wtail, std::max<int64_t>(1, pl->nwarps));
     }
     UP(tiles, hp.tiles);
     UP(wins, hp.wins);
@@ -1029,40 +1537,57 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         std::vector<int32_t> inv(lo.forward.size());
         for (size_t i = 0; i < inv.size(); i++) inv[lo.forward[i]] = (int32_t)i;
         UP(iperm, inv);
-        if (cudaMalloc((void **)&pl->xs, sizeof(double) * (size_t)pl->n) != cudaSuccess ||
-            cudaMalloc((void **)&pl->ys, sizeof(double) * (size_t)pl->n) != cudaSuccess) {
+        ZALLOC(xs, pl->n);
+        ZALLOC(ys, pl->n);
+    }
+    ZALLOC(gs, 1);
+    ZALLOC(part, kDotGrid);
+    {
+        GState g0{};
+        g0.xe = kXeNone;
+        g0.xe_seen = kXeNone;
+        if (cudaMemcpy(pl->gs, &g0, sizeof(g0), cudaMemcpyHostToDevice) != cudaSuccess) {
             delete pl;
-            PARS3_FAIL(PARS3_ERR_CUDA, "cudaMalloc failed");
+            PARS3_FAIL(PARS3_ERR_CUDA, "cudaMemcpy failed");
         }
-        pl->bytes += 2 * sizeof(double) * pl->n;
+    }
+    if (grid_ok) {
+        pl->ev_g = G.ev_g;
+        pl->hgrid = G.hgrid;
+        pl->cmax = G.cmax;
+        ZALLOC(blk_dot, std::max<int64_t>(pl->ntiles, kDotGrid));
+        ZALLOC(blk_max, std::max<int64_t>(pl->ntiles, kDotGrid));
+        ZALLOC(yacc, pl->n);
     }
 #undef UP
-    if (cudaMalloc((void **)&pl->counter, 2 * sizeof(int32_t)) != cudaSuccess ||  // claims, status
-        cudaMemset(pl->counter, 0, 2 * sizeof(int32_t)) != cudaSuccess) {
-        delete pl;
-        PARS3_FAIL(PARS3_ERR_CUDA, "cudaMalloc failed");
-    }
+#undef ZALLOC
     pl->smem = pl->words == 0 ? Layout<0>::kSmem : pl->words == 2 ? Layout<2>::kSmem : Layout<3>::kSmem;
     // the attribute is per function, shared by every plan: set it to the
     // function's fixed layout size
     cudaError_t e = cudaSuccess;
     {
-        const void *fns[6] = {(const void *)k_tiles<0, false>, (const void *)k_tiles<2, false>,
-                              (const void *)k_tiles<3, false>, (const void *)k_tiles<0, true>,
-                              (const void *)k_tiles<2, true>,  (const void *)k_tiles<3, true>};
+        const void *fns[10] = {
+            (const void *)k_tiles<0, false, false>, (const void *)k_tiles<2, false, false>,
+            (const void *)k_tiles<3, false, false>, (const void *)k_tiles<0, true, false>,
+            (const void *)k_tiles<2, true, false>,  (const void *)k_tiles<3, true, false>,
+            (const void *)k_tiles<0, false, true>,  (const void *)k_tiles<2, false, true>,
+            (const void *)k_tiles<3, false, true>,  (const void *)k_finish};
         const int sm[3] = {Layout<0>::kSmem, Layout<2>::kSmem, Layout<3>::kSmem};
-        for (int f = 0; f < 6 && e == cudaSuccess; f++)
-            e = cudaFuncSetAttribute(fns[f], cudaFuncAttributeMaxDynamicSharedMemorySize, sm[f % 3]);
+        for (int f = 0; f < 10 && e == cudaSuccess; f++)
+            e = cudaFuncSetAttribute(fns[f], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     f == 9 ? kFinishSmem : sm[f % 3]);
     }
-    int per_sm = 0, sms = 0, dev = 0;
+    int per_sm = 0, per_sm_redo = 0, sms = 0, dev = 0;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, pl->words == 0 ? k_tiles<0, false> : pl->words == 2 ? k_tiles<2, false> : k_tiles<3, false>,
-            kThreads,
-            pl->smem);
-    if (e != cudaSuccess || per_sm < 1) {
+            &per_sm, pl->words == 0 ? k_tiles<0, false, true> : pl->words == 2 ? k_tiles<2, false, true> : k_tiles<3, false, true>,
+            kThreads, pl->smem);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm_redo, k_finish, kThreads, kFinishSmem);
+    if (e != cudaSuccess || per_sm < 1 || per_sm_redo < 1) {
         delete pl;
         PARS3_FAIL(PARS3_ERR_CUDA, "tile kernel cannot be resident (smem %zu B): %s", pl->smem,
                    cudaGetErrorString(e));
@@ -1070,40 +1595,126 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     pl->grid = per_sm * sms;
     if (max_ctas > 0 && pl->grid > max_ctas) pl->grid = max_ctas;
     if (pl->grid > pl->ntiles) pl->grid = pl->ntiles > 0 ? pl->ntiles : 1;
+    pl->grid_redo = std::min(pl->grid, per_sm_redo * sms);
     *out = pl;
     return PARS3_OK;
 }
 
-static int launch_tiles(pars3_plan *pl, const double *x, double *y, bool zero_y, cudaStream_t st) {
-    if (pl->direct) {
-        if (pl->n == 0) return PARS3_OK;
-        const int grid = (int)std::min<int64_t>(148 * 4, (pl->n + 511) / 512);
-        k_direct_init<<<grid, 512, 0, st>>>((int32_t)pl->n, pl->diag_const ? nullptr : pl->diag,
-                                            pl->diag_alpha, x, y, zero_y ? 0 : 1);
-        LAUNCH_CHECK();
-        const int run = pl->direct_run;
-        const int64_t runs = (pl->dm + run - 1) / run;
-        const int grid2 = (int)std::min<int64_t>(148 * 16, (runs + 255) / 256);
-        if (grid2 > 0) {
-            auto fn = run == 4 ? k_direct<4> : run == 16 ? k_direct<16> : k_direct<8>;
-            fn<<<grid2, 256, 0, st>>>(pl->dm, pl->drow, pl->dcol, pl->dval, x, y);
-            LAUNCH_CHECK();
-        }
-        return PARS3_OK;
-    }
-    if (zero_y && pl->n > 0) CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)pl->n, st));
+static DevPlan dev_plan(const pars3_plan *pl) {
+    DevPlan P{};
+    P.tiles = pl->tiles;
+    P.wins = pl->wins;
+    P.slice_off = pl->slice_off;
+    P.rec = pl->rec;
+    P.ucol = pl->ucol;
+    P.diag = pl->diag;
+    P.ntiles = pl->ntiles;
+    P.watchdog = pl->watchdog;
+    P.diag_const = pl->diag_const;
+    P.diag_alpha = pl->diag_alpha;
+    P.phase_clk = pl->phase_clk;
+    P.pf = pl->pf;
+    P.pf_dist = pl->pf_dist;
+    P.peers = pl->peers;
+    P.gs = pl->gs;
+    P.blk_dot = pl->blk_dot;
+    P.blk_max = pl->blk_max;
+    P.yacc = pl->yacc;
+    P.ev_g = pl->ev_g;
+    P.hgrid = pl->hgrid;
+    P.cmax = pl->cmax;
+    return P;
+}
+
+// RED form over the tiles: y (+)= A x with fp64 reductions (peer mode, y +=
+// A x, plans without the grid form).  y zeroed first unless `acc`.  The
+// claim counter is zero between products (k_finish resets it after a grid
+// product, this launch after its own).
+static int launch_red(pars3_plan *pl, const double *x, double *y, bool acc, cudaStream_t st) {
+    if (!acc && pl->n > 0) CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)pl->n, st));
     if (pl->ntiles == 0) return PARS3_OK;
-    CUDA_TRY(cudaMemsetAsync(pl->counter, 0, 2 * sizeof(int32_t), st));
-    DevPlan P{pl->tiles,      pl->wins,       pl->slice_off, pl->rec,       pl->ucol,
-              pl->diag,       pl->counter,    pl->ntiles,    pl->watchdog,  pl->diag_const,
-              pl->diag_alpha, pl->phase_clk,  pl->pf,        pl->pf_dist,  pl->peers};
+    const DevPlan P = dev_plan(pl);
     const bool peer = pl->peers.nranks > 0;
     if (pl->words == 0)
-        (peer ? k_tiles<0, true> : k_tiles<0, false>)<<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
+        (peer ? k_tiles<0, true, false> : k_tiles<0, false, false>)<<<pl->grid, kThreads, pl->smem, st>>>(
+            P, x, y, nullptr, nullptr, 0);
     else if (pl->words == 2)
-        (peer ? k_tiles<2, true> : k_tiles<2, false>)<<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
+        (peer ? k_tiles<2, true, false> : k_tiles<2, false, false>)<<<pl->grid, kThreads, pl->smem, st>>>(
+            P, x, y, nullptr, nullptr, 0);
     else
-        (peer ? k_tiles<3, true> : k_tiles<3, false>)<<<pl->grid, kThreads, pl->smem, st>>>(P, x, y);
+        (peer ? k_tiles<3, true, false> : k_tiles<3, false, false>)<<<pl->grid, kThreads, pl->smem, st>>>(
+            P, x, y, nullptr, nullptr, 0);
+    LAUNCH_CHECK();
+    CUDA_TRY(cudaMemsetAsync(&pl->gs->claim, 0, sizeof(int32_t), st));
+    return PARS3_OK;
+}
+
+// GRID form: y = A x written by the block finalizers, *dot = <y, w> fused
+// when w is y (dot_self) or given, by k_finish (which redoes flagged products)
+static int launch_grid(pars3_plan *pl, const double *x, double *y, const double *w, double *dot,
+                       bool dot_self, cudaStream_t st) {
+    if (!pl->xe_ready) {  // first product: the scale bound from a pass over x
+        const int grid = (int)std::min<int64_t>(148 * 4, (pl->n + 511) / 512);
+        k_xmax<<<grid, 512, 0, st>>>((int32_t)pl->n, x, pl->gs);
+        LAUNCH_CHECK();
+        pl->xe_ready = 1;
+    }
+    const DevPlan P = dev_plan(pl);
+    const int ds = dot_self ? 1 : 0;
+    if (pl->words == 0)
+        k_tiles<0, false, true><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, w, dot, ds);
+    else if (pl->words == 2)
+        k_tiles<2, false, true><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, w, dot, ds);
+    else
+        k_tiles<3, false, true><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, w, dot, ds);
+    LAUNCH_CHECK();
+    int32_t n32 = (int32_t)pl->n;
+    void *args[] = {(void *)&P, (void *)&x, (void *)&y, (void *)&w, (void *)&dot, (void *)&ds, (void *)&n32};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_finish, dim3(pl->grid_redo), dim3(kThreads), args,
+                                         kFinishSmem, st));
+    return PARS3_OK;
+}
+
+__global__ void __launch_bounds__(512) k_add(int32_t n, const double *__restrict__ a, double *y) {
+    const int32_t stride = gridDim.x * blockDim.x;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) y[i] += a[i];
+}
+
+// row-major form: y = A x (k_csr + k_csr_fix); y += A x through a scratch
+static int launch_direct(pars3_plan *pl, const double *x, double *y, bool acc, cudaStream_t st) {
+    if (pl->n == 0) return PARS3_OK;
+    double *out = y;
+    if (acc) {
+        if (!pl->yacc_tmp) CUDA_TRY(cudaMalloc((void **)&pl->yacc_tmp, sizeof(double) * (size_t)pl->n));
+        out = pl->yacc_tmp;
+    }
+    const int grid = (int)std::min<int64_t>(148 * 2, (pl->nwarps + 7) / 8);
+    k_csr<<<grid, 256, 0, st>>>(pl->ne, pl->nwarps, pl->ccol, pl->cval, pl->clrow, pl->clflags, x, out,
+                                pl->whead, pl->wtail);
+    LAUNCH_CHECK();
+    if (pl->nspan > 0) {
+        k_csr_fix<<<(pl->nspan + 255) / 256, 256, 0, st>>>(pl->nspan, pl->span_row, pl->span_w0, pl->span_w1,
+                                                          pl->whead, pl->wtail, out);
+        LAUNCH_CHECK();
+    }
+    if (acc) {
+        const int g = (int)std::min<int64_t>(148 * 4, (pl->n + 511) / 512);
+        k_add<<<g, 512, 0, st>>>((int32_t)pl->n, out, y);
+        LAUNCH_CHECK();
+    }
+    return PARS3_OK;
+}
+
+// deterministic <a, b> into *out (part: kDotGrid doubles of scratch)
+static int launch_dot(int64_t n, const double *a, const double *b, double *part, double *out, cudaStream_t st) {
+    if (n == 0) {
+        CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
+        return PARS3_OK;
+    }
+    if (((uintptr_t)a | (uintptr_t)b) & 15) PARS3_FAIL(PARS3_ERR_ARG, "vectors must be 16-byte aligned");
+    k_dot<<<kDotGrid, 512, 0, st>>>((int32_t)n, a, b, part);
+    LAUNCH_CHECK();
+    k_sum_parts<<<1, kThreads, 0, st>>>(kDotGrid, part, out);
     LAUNCH_CHECK();
     return PARS3_OK;
 }
@@ -1142,27 +1753,39 @@ extern "C" int pars3_plan_set_peers(pars3_plan *pl, int32_t nranks, int32_t me, 
 // internal copies xs / ys and the epilogue gathers y (and the dot) back
 static int plan_product(pars3_plan *pl, const double *x, double *y, bool acc, const double *w,
                         double *dot, cudaStream_t st) {
-    if (dot) CUDA_TRY(cudaMemsetAsync(dot, 0, sizeof(double), st));
+    if (pl->n > 0 && x == y) PARS3_FAIL(PARS3_ERR_ARG, "x and y must not alias");
+    const bool grid = pl->grid_ok && !acc && pl->peers.nranks == 0 && pl->ntiles > 0;
     if (!pl->perm) {
-        int rc = launch_tiles(pl, x, y, !acc, st);
-        if (rc || !dot || pl->n == 0) return rc;
-        // 16-byte loads need 16-byte aligned vectors (torch allocations are)
-        if (((uintptr_t)y | (uintptr_t)w) & 15) PARS3_FAIL(PARS3_ERR_ARG, "y and w must be 16-byte aligned");
-        k_dot<<<148 * 4, 512, 0, st>>>((int32_t)pl->n, y, w, dot);
-        LAUNCH_CHECK();
-        return PARS3_OK;
+        if (pl->direct) {
+            int rc = launch_direct(pl, x, y, acc, st);
+            if (rc || !dot) return rc;
+            return launch_dot(pl->n, y, w, pl->part, dot, st);
+        }
+        if (grid) return launch_grid(pl, x, y, w, dot, dot && w == y, st);
+        int rc = launch_red(pl, x, y, acc, st);
+        if (rc || !dot) return rc;
+        return launch_dot(pl->n, y, w, pl->part, dot, st);
     }
     const int32_t n = (int32_t)pl->n;
-    const int grid = (int)std::min<int64_t>(148 * 4, (pl->n + 511) / 512);
-    k_perm_in<<<grid, 512, 0, st>>>(n, pl->iperm, x, pl->xs);
+    const int g = (int)std::min<int64_t>(148 * 4, (pl->n + 511) / 512);
+    k_perm_in<<<g, 512, 0, st>>>(n, pl->iperm, x, pl->xs);
     LAUNCH_CHECK();
-    int rc = launch_tiles(pl, pl->xs, pl->ys, true, st);
+    // <y, y> = <ys, ys>: fused into the grid pass; another w goes through
+    // the gather's epilogue
+    const bool fused = grid && dot && w == y;
+    int rc = grid ? launch_grid(pl, pl->xs, pl->ys, fused ? pl->ys : nullptr, fused ? dot : nullptr, fused, st)
+                  : launch_red(pl, pl->xs, pl->ys, false, st);
     if (rc) return rc;
+    const bool pdot = dot && !fused;
     if (acc)
-        (dot ? k_perm_out<true, true> : k_perm_out<true, false>)<<<grid, 512, 0, st>>>(n, pl->perm, pl->ys, y, w, dot);
+        (pdot ? k_perm_out<true, true> : k_perm_out<true, false>)<<<g, 512, 0, st>>>(n, pl->perm, pl->ys, y, w, pl->part);
     else
-        (dot ? k_perm_out<false, true> : k_perm_out<false, false>)<<<grid, 512, 0, st>>>(n, pl->perm, pl->ys, y, w, dot);
+        (pdot ? k_perm_out<false, true> : k_perm_out<false, false>)<<<g, 512, 0, st>>>(n, pl->perm, pl->ys, y, w, pl->part);
     LAUNCH_CHECK();
+    if (pdot) {
+        k_sum_parts<<<1, kThreads, 0, st>>>(g, pl->part, dot);
+        LAUNCH_CHECK();
+    }
     return PARS3_OK;
 }
 
@@ -1185,31 +1808,43 @@ extern "C" int pars3_plan_spmv_dot(pars3_plan *pl, const double *x, double *y, c
 extern "C" int pars3_dot(int64_t n, const double *a, const double *b, double *out, void *stream) {
     if (n < 0 || n >= INT32_MAX || !out || (n > 0 && (!a || !b))) PARS3_FAIL(PARS3_ERR_ARG, "bad argument");
     cudaStream_t st = (cudaStream_t)stream;
-    CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
-    if (n == 0) return PARS3_OK;
-    if (((uintptr_t)a | (uintptr_t)b) & 15) PARS3_FAIL(PARS3_ERR_ARG, "a and b must be 16-byte aligned");
-    k_dot<<<148 * 4, 512, 0, st>>>((int32_t)n, a, b, out);
-    LAUNCH_CHECK();
-    return PARS3_OK;
+    // stream-ordered scratch for the per-block shares (pool allocation)
+    double *part = nullptr;
+    CUDA_TRY(cudaMallocAsync((void **)&part, sizeof(double) * kDotGrid, st));
+    const int rc = launch_dot(n, a, b, part, out, st);
+    CUDA_TRY(cudaFreeAsync(part, st));
+    return rc;
 }
 
 extern "C" int pars3_plan_status(pars3_plan *pl, int32_t *flags, void *stream) {
     if (!pl || !flags) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
     *flags = 0;
-    if (!pl->counter) return PARS3_OK;
+    if (!pl->gs) return PARS3_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    CUDA_TRY(cudaMemcpyAsync(flags, pl->counter + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    GState g{};
+    CUDA_TRY(cudaMemcpyAsync(&g, pl->gs, sizeof(g), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (g.redone != pl->seen_redone) *flags |= 1;
+    if (g.fp64_tiles != pl->seen_fp64_tiles) *flags |= 2;
+    pl->seen_redone = g.redone;
+    pl->seen_fp64_tiles = g.fp64_tiles;
     return PARS3_OK;
 }
 
 extern "C" int pars3_plan_kernel_count(const pars3_plan *pl, int32_t with_dot, int32_t *count) {
     if (!pl || !count) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
-    if (pl->direct)
-        *count = (pl->n > 0 ? 1 : 0) + (pl->dm > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 1 : 0);
-    else
-        *count = pl->perm ? (pl->ntiles > 0 ? 3 : 2)
-                          : (pl->ntiles > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 1 : 0);
+    const bool grid = pl->grid_ok && pl->peers.nranks == 0 && pl->ntiles > 0;
+    int c = 0;
+    if (pl->direct) {
+        c = (pl->n > 0 ? 1 : 0) + (pl->nspan > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 2 : 0);
+    } else if (pl->perm) {
+        c = 2 + (pl->ntiles > 0 ? (grid ? 2 : 1) : 0);
+    } else if (grid) {
+        c = 2;
+    } else {
+        c = (pl->ntiles > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 2 : 0);
+    }
+    *count = c;
     return PARS3_OK;
 }
 
@@ -1235,6 +1870,10 @@ extern "C" int pars3_plan_stats(const pars3_plan *pl, int64_t *stats) {
     stats[11] = pl->local_slots;
     stats[12] = pl->dropped;
     stats[13] = pl->direct;
+    stats[14] = pl->grid_ok;
+    stats[15] = pl->hgrid;
+    stats[16] = pl->cmax;
+    stats[17] = pl->ev_g;
     return PARS3_OK;
 }
 

@@ -52,10 +52,6 @@ class Pars3Operator:
                     outer_row=_c(outer_row, np.int32), outer_col=_c(outer_col, np.int32),
                     outer_val=_c(outer_val, np.float64))
         self.nnz = int(host["mid_col"].size + host["outer_col"].size)
-        # the source arrays (references, no copy) for an fp64 twin (fallback())
-        self._src = (n, beta, diag, mid_ptr, mid_col, mid_val, outer_row, outer_col, outer_val, p,
-                     block_start, options)
-        self._fallback = None
         view = _lib.SplitView(self.n, self.beta, _lib.ptr(host["diag"]), _lib.ptr(host["mid_ptr"]),
                               _lib.ptr(host["mid_col"]), _lib.ptr(host["mid_val"]),
                               int(host["outer_col"].size), _lib.ptr(host["outer_row"]),
@@ -143,9 +139,6 @@ class Pars3Operator:
         pl["ev_out"][b].record(d2h)
         if not non_blocking:
             pl["ev_out"][b].synchronize()
-            if self.status(comp):  # inexact for these x values: redo with the fp64 twin
-                xd = x.to(self.device)
-                out.copy_(self.fallback().matvec(xd))
         return out
 
     def host_join(self, stream=None):
@@ -162,33 +155,16 @@ class Pars3Operator:
             pl["d2h"].synchronize()
 
     def status(self, stream=None) -> int:
-        """Flags of the last product (synchronises the stream): 1 when an x
-        value fell outside what the exact fixed-point accumulation carries
-        (non-finite, subnormal, extreme range); the product must then be
-        redone with ``fallback()``."""
+        """Flags since the previous call (synchronises the stream).  Every
+        product is exact whatever the input; these say
+        how it got there: bit 0 -- a product was redone by the fp64 pass
+        (non-finite x, x beyond the grid's bound, or a grid too coarse for
+        the result), so it is exact but not bitwise repeatable; bit 1 -- some
+        tiles accumulated in fp64 (the per-tile guard)."""
         f = ctypes.c_int32()
         _lib.check(self._L.pars3_plan_status(self._handle, ctypes.byref(f), _lib.stream_ptr(stream)),
                    "pars3_plan_status")
         return int(f.value)
-
-    def fallback(self):
-        """The same operator with fp64 shared accumulators (mode 2): IEEE
-        semantics for non-finite and extreme inputs."""
-        if self._fallback is None:
-            (n, beta, diag, mp, mc, mv, orow, ocol, oval, p, bs, options) = self._src
-            o = tuple(options or ()) + (0, 0, 0, -1, 0, 0, 0)[len(options or ()):]
-            self._fallback = Pars3Operator(n, beta, diag, mp, mc, mv, orow, ocol, oval, p=p,
-                                           block_start=bs, device=self.device,
-                                           options=o[:4] + (2,) + o[5:])
-        return self._fallback
-
-    def checked_matvec(self, x, y=None):
-        """matvec, redone with the fp64 twin when status() flags the result
-        (blocking: used by the numpy / host-tensor entry points)."""
-        y = self.matvec(x, y)
-        if self.status():
-            y = self.fallback().matvec(x, y)
-        return y
 
     def kernel_count(self, with_dot: bool = False) -> int:
         c = ctypes.c_int32()
@@ -201,11 +177,11 @@ class Pars3Operator:
         return int(b.value)
 
     def stats(self) -> dict:
-        a = np.zeros(14, dtype=np.int64)
+        a = np.zeros(18, dtype=np.int64)
         _lib.check(self._L.pars3_plan_stats(self._handle, _lib.ptr(a)))
         keys = ("tiles", "slices", "padded_slots", "entries", "windows", "max_local", "grid",
                 "device_bytes", "list_tiles", "accum_words", "locality_order", "local_slots",
-                "locality_dropped", "direct")
+                "locality_dropped", "direct", "grid_form", "grid_hbits", "grid_cmax", "grid_ev")
         return {k: int(v) for k, v in zip(keys, a)}
 
     def close(self):
