@@ -22,7 +22,12 @@ flush is needed between steps.
 --impl reference times the reference algorithm on the host cores instead:
 the C restatement of the reference's _pars3 kernel (oracle/oracle.c,
 OpenMP, p = all host cores), the reference package itself being a numba
-library that is not shipped to the GPU box.
+library that is not shipped to the GPU box.  Its inputs come through the
+oracle's own chain only (pattern, RCM, relabel, split, classify: no
+libpars3 in that process), and its line carries the GPU arm's config.
+
+--gpus N without a torchrun environment re-launches this script under
+torch.distributed.run with N processes (one per GPU, 127.0.0.1 rendezvous).
 """
 
 from __future__ import annotations
@@ -64,8 +69,54 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def golden_hashes():
+    path = os.path.join(ROOT, "tests", "golden", "hashes.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def check_labels(cfg: str, forward, chain: str):
+    """Refuse to time a product whose RCM labels differ from the reference's
+    (tests/golden/hashes.json: make_golden.py ran the reference's rcm_order
+    on the same seeded input)."""
+    import hashlib
+
+    import numpy as np
+    h = golden_hashes().get(cfg, {}).get("rcm_forward")
+    if h is None and cfg == "c1":  # c1's reference outputs are stored whole
+        try:
+            ref = np.load(os.path.join(ROOT, "tests", "golden", "c1.npz"))["rcm_forward"]
+            h = hashlib.sha256(np.ascontiguousarray(ref, dtype=np.int64).tobytes()).hexdigest()
+        except Exception:
+            h = None
+    if h is None:
+        log(f"{cfg}: no golden RCM hash (not checked)")
+        return None
+    got = hashlib.sha256(np.ascontiguousarray(forward, dtype=np.int64).tobytes()).hexdigest()
+    if got != h:
+        raise SystemExit(f"[bench] {cfg}: the {chain} chain's RCM labels differ from the reference's "
+                         f"(sha256 {got[:16]} != {h[:16]}): not timing a product on them")
+    log(f"{cfg}: {chain} chain RCM labels == the reference's (sha256 {h[:16]})")
+    return True
+
+
+def config_dict(cfg, n, nnz, beta, bw, world):
+    """The workload description both arms print (same keys, same values)."""
+    B = algorithmic_bytes(n, nnz)
+    return {"workload": cfg, "n": n, "nnz_lower": nnz, "beta": beta, "rcm_bandwidth": bw,
+            "step": "y = A x fused with <y, y>", "bytes_per_spmv": B,
+            "flops_per_spmv": algorithmic_flops(n, nnz),
+            "l2": (f"inputs larger than L2 ({B / 1e9:.2f} GB per SpMV, 126 MB L2): no flush needed"
+                   if B > 126e6 else f"L2-resident ({B / 1e6:.1f} MB per SpMV): reported, not an HBM claim"),
+            "parallelism": f"row blocks x{world} (partition_rows)" if world > 1 else "single GPU"}
+
+
 def build_problem(cfg: str, beta=None, use_gpu=True):
-    """Generator -> pattern -> RCM -> relabel -> split (native pipeline)."""
+    """Generator -> pattern -> RCM -> relabel -> split (native pipeline); the
+    RCM labels are checked against the reference's before anything is timed."""
     import numpy as np
 
     import paper_2407_17651_b200 as P
@@ -99,6 +150,7 @@ def build_problem(cfg: str, beta=None, use_gpu=True):
         s = P.split_bands(m, beta)
         t3 = time.time()
     del m0
+    check_labels(cfg, perm.forward, "GPU" if gpu else "host")
     x = G.make_x(m.n, G.CONFIGS[cfg]["seed_x"])
     log(f"{cfg}: n={m.n} m={m.nnz_offdiag} rcm_bw={bw} beta={beta} mid={s.middle_count} "
         f"outer={s.outer_count}; gen {t1 - t0:.1f}s preprocessing on the "
@@ -260,22 +312,47 @@ def cpu_baseline(s, x, n, m, reps_max=10, min_seconds=10.0, mat=None, bw=None):
     return out
 
 
+def oracle_problem(cfg, beta=None):
+    """The reference arm's inputs, through the oracle's chain only (no
+    libpars3): generator -> oracle.pattern_from_sss -> oracle.rcm_order ->
+    oracle.permute_sss -> oracle.split_bands -> oracle.classify_conflicts
+    (the C / numpy restatements of reorder.py:103-297, split.py:116-361,
+    pinned to the reference by tests/test_config_hashes.py)."""
+    from oracle import oracle as O
+    from paper_2407_17651_b200 import generators as G
+    t0 = time.time()
+    g = G.make_config(cfg)
+    ip, ix = O.pattern_from_sss(g.n, g.row_ptr, g.col_ind)
+    fw = O.rcm_order(g.n, ip, ix)
+    del ip, ix
+    check_labels(cfg, fw, "oracle")
+    rp, ci, od, dg = O.permute_sss(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags, fw)
+    n, nnz = g.n, int(ci.size)
+    del g, fw
+    bw = O.compute_bandwidth(n, rp, ci)
+    if beta is None:
+        beta = O.default_beta(n, bw)
+    split = O.split_bands(n, rp, ci, od, dg, beta)
+    x = G.make_x(n, G.CONFIGS[cfg]["seed_x"])
+    log(f"{cfg}: n={n} m={nnz} rcm_bw={bw} beta={beta} oracle chain {time.time() - t0:.1f}s")
+    return n, nnz, bw, beta, split, x
+
+
 def run_reference(args):
-    """--impl reference: the reference algorithm on the host cores (rank 0)."""
+    """--impl reference: the reference algorithm on the host cores (rank 0
+    only; other ranks exit without work)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"[bench] WORLD_SIZE {world} != --gpus {args.gpus}")
     if rank != 0:
         return
-    # host-native chain (bit-identical inputs), no CUDA in the reference arm
-    m, s, bw, beta, x = build_problem(args.config, args.beta, use_gpu=False)
-    import numpy as np
-
-    from oracle import oracle as O
     cores = len(os.sched_getaffinity(0))
+    os.environ["OMP_NUM_THREADS"] = str(cores)  # (torchrun sets 1; read when libgomp loads)
+    from oracle import oracle as O
+    n, nnz, bw, beta, split, x = oracle_problem(args.config, args.beta)
     O.build()
-    split = {"n": s.n, "beta": s.beta, "mid_ptr": s.mid_ptr, "mid_col": s.mid_col.astype(np.int64),
-             "mid_val": s.mid_val, "diag": s.diag, "outer_row": s.outer_row.astype(np.int64),
-             "outer_col": s.outer_col.astype(np.int64), "outer_val": s.outer_val}
-    plan = O.classify_conflicts(split, O.partition_rows(s.n, cores))
+    plan = O.classify_conflicts(split, O.partition_rows(n, cores))
     for _ in range(args.warmup):
         O.spmv_pars3(split, plan, x, nthreads=cores)
     t0 = time.perf_counter()
@@ -283,19 +360,18 @@ def run_reference(args):
         y = O.spmv_pars3(split, plan, x, nthreads=cores)
         float(y @ y)  # the step's inner product
     dt = (time.perf_counter() - t0) / args.steps
-    n, nnz = m.n, m.nnz_offdiag
     val = algorithmic_bytes(n, nnz) / dt / 1e9
     out = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded generator, BASELINE config)",
-        "config": {"workload": args.config, "n": n, "nnz_lower": nnz, "beta": beta,
-                   "rcm_bandwidth": bw, "p": cores},
+        "data": "synthetic (seeded generator, BASELINE config; random-init values U(-1,1))",
+        "config": config_dict(args.config, n, nnz, beta, bw, args.gpus),
         "gflops": algorithmic_flops(n, nnz) / dt / 1e9,
         "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full SpMV + dot steps (oracle C _pars3 "
-                                   f"restatement, p={cores})"},
+                         "sample": f"{args.steps} full SpMV + dot steps (oracle C _pars3 restatement of "
+                                   f"parallel.py:60-120, p={cores}, OpenMP {cores} threads; inputs from "
+                                   f"the oracle chain)"},
         "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -309,6 +385,8 @@ def run_gpu(args):
     from oracle import oracle as O
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"[bench] WORLD_SIZE {world} != --gpus {args.gpus}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     local = local % torch.cuda.device_count()
@@ -416,6 +494,9 @@ def run_gpu(args):
         barrier()
     step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
 
+    # the product's kernels alone, per phase (CUDA events on the stream,
+    # pars3_plan_profile): main kernel (tiles / full CSR) and finish
+    phases = op.profile(x, ybuf, with_dot=False, reps=args.steps) if world == 1 else None
     # dominant kernel: the local SpMV alone (every local part at N > 1), same
     # clock discipline
     peer = dist is not None and hasattr(dop, "local_product")
@@ -476,9 +557,10 @@ def run_gpu(args):
     achieved = B_rank / (spmv_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and world == 1:
         try:
-            traffic = json.load(open(tpath)).get(args.config) if world == 1 else None
+            tj = json.load(open(tpath)).get(args.config)
+            traffic = tj.get("bytes") if isinstance(tj, dict) else tj
         except Exception:
             traffic = None
     if rank != 0:
@@ -493,23 +575,17 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, BASELINE config; random-init values U(-1,1))",
-        "config": {"workload": args.config, "n": n, "nnz_lower": nnz, "beta": beta,
-                   "rcm_bandwidth": bw, "step": "y = A x fused with <y, y>",
-                   "bytes_per_spmv": B, "flops_per_spmv": F,
-                   "l2": (f"inputs larger than L2 (device plan {stats['device_bytes'] / 1e9:.2f} GB "
-                          "streamed per step, 126 MB L2): no flush needed"
-                          if stats["device_bytes"] * world > 126e6 else
-                          f"L2-resident (plan {stats['device_bytes'] / 1e6:.1f} MB): reported, not an "
-                          "HBM claim"),
-                   "parallelism": (f"row blocks x{world} (partition_rows), " + (
-                       "halo + accumulation inside the kernel over NVLink peer memory"
-                       if stats.get("dist_mode") == "peer" else "NCCL halo + accumulation exchange")
-                       if world > 1 else "single GPU")},
+        "config": config_dict(args.config, n, nnz, beta, bw, world),
         "gflops": F / (step_ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel_ms": spmv_ms, "frac_of_8TBs": achieved / 8000.0,
-                     "bytes_per_launch": B_rank},
+                     "bytes_per_launch": B_rank,
+                     "kernels": ("the product: the main kernel (tile kernel, or full CSR) and its finish "
+                                 "(k_finish: the grid accumulator -> fp64 y; or the row fix-up); achieved = "
+                                 "algorithmic bytes / their time together" if world == 1 else
+                                 "each rank's local product"),
+                     "phases_ms": phases},
         "cpu_baseline": cpu,
         "e2e": {"value": B / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms,
@@ -545,6 +621,17 @@ def main():
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (127.0.0.1 rendezvous)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node",
+               str(args.gpus), "--master-addr", "127.0.0.1", "--master-port", str(port),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        log("re-launching under torch.distributed.run:", " ".join(cmd[3:9]))
+        raise SystemExit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -188,6 +188,14 @@ int pars3_full_csr_host(const pars3_split_view *split, int64_t *sizes, int32_t *
                         int32_t *lane_row, uint32_t *lane_flags, int32_t *span_row, int32_t *span_w0,
                         int32_t *span_w1);
 
+/* Phase times (CUDA events on `stream`) averaged over `reps` products y = A x
+ * (with <y, y> when with_dot): ms[0] the main kernel (tile kernel or full
+ * CSR; a locality plan's gather of x included), ms[1] the next phase
+ * (k_finish, the span fix-up, or the RED form's dot), ms[2] the rest,
+ * ms[3] the whole product.  For the bench's roofline breakdown. */
+int pars3_plan_profile(pars3_plan *plan, const double *x, double *y, int32_t with_dot, int32_t reps,
+                       double *ms, void *stream);
+
 /* Number of libpars3 kernels one pars3_plan_spmv (with_dot = 0) or
  * pars3_plan_spmv_dot (with_dot = 1) call launches (memsets excluded). */
 int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *count);

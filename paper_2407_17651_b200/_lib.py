@@ -76,6 +76,7 @@ _SIGS = {
     "pars3_plan_stats": (ctypes.c_int, [_vp, _vp]),
     "pars3_locality_order": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, ctypes.POINTER(_c_i64)]),
     "pars3_full_csr_host": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pars3_plan_profile": (ctypes.c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _vp, _vp]),
     "pars3_plan_status": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i32), _vp]),
     "pars3_plan_kernel_count": (ctypes.c_int, [_vp, _c_i32, ctypes.POINTER(_c_i32)]),
     "pars3_plan_destroy": (ctypes.c_int, [_vp]),

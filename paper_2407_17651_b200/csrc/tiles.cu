@@ -1199,6 +1199,8 @@ struct pars3_plan {
     double *blk_dot = nullptr, *blk_max = nullptr, *part = nullptr;
     long long *yacc = nullptr;
     int32_t seen_fp64_tiles = 0, seen_redone = 0;  // pars3_plan_status: counters at its last call
+    cudaEvent_t *prof = nullptr;  // pars3_plan_profile: events at the product's phase boundaries
+    int prof_k = 0;
     // internal locality order (locality.cpp): the tiles hold P A P^T, x and
     // y pass through perm (split label -> internal label) and xs / ys
     int32_t *perm = nullptr, *iperm = nullptr;
@@ -1626,6 +1628,11 @@ static DevPlan dev_plan(const pars3_plan *pl) {
     return P;
 }
 
+// pars3_plan_profile: record the next phase-boundary event
+static void mark(pars3_plan *pl, cudaStream_t st) {
+    if (pl->prof && pl->prof_k < 4) cudaEventRecord(pl->prof[pl->prof_k++], st);
+}
+
 // RED form over the tiles: y (+)= A x with fp64 reductions (peer mode, y +=
 // A x, plans without the grid form).  y zeroed first unless `acc`.  The
 // claim counter is zero between products (k_finish resets it after a grid
@@ -1645,6 +1652,7 @@ static int launch_red(pars3_plan *pl, const double *x, double *y, bool acc, cuda
         (peer ? k_tiles<3, true, false> : k_tiles<3, false, false>)<<<pl->grid, kThreads, pl->smem, st>>>(
             P, x, y, nullptr, nullptr, 0);
     LAUNCH_CHECK();
+    mark(pl, st);
     CUDA_TRY(cudaMemsetAsync(&pl->gs->claim, 0, sizeof(int32_t), st));
     return PARS3_OK;
 }
@@ -1668,6 +1676,7 @@ static int launch_grid(pars3_plan *pl, const double *x, double *y, const double 
     else
         k_tiles<3, false, true><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, w, dot, ds);
     LAUNCH_CHECK();
+    mark(pl, st);
     int32_t n32 = (int32_t)pl->n;
     void *args[] = {(void *)&P, (void *)&x, (void *)&y, (void *)&w, (void *)&dot, (void *)&ds, (void *)&n32};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_finish, dim3(pl->grid_redo), dim3(kThreads), args,
@@ -1692,6 +1701,7 @@ static int launch_direct(pars3_plan *pl, const double *x, double *y, bool acc, c
     k_csr<<<grid, 256, 0, st>>>(pl->ne, pl->nwarps, pl->ccol, pl->cval, pl->clrow, pl->clflags, x, out,
                                 pl->whead, pl->wtail);
     LAUNCH_CHECK();
+    mark(pl, st);
     if (pl->nspan > 0) {
         k_csr_fix<<<(pl->nspan + 255) / 256, 256, 0, st>>>(pl->nspan, pl->span_row, pl->span_w0, pl->span_w1,
                                                           pl->whead, pl->wtail, out);
@@ -1751,9 +1761,20 @@ extern "C" int pars3_plan_set_peers(pars3_plan *pl, int32_t nranks, int32_t me, 
 
 // one product through the plan; with a locality order the tiles run on the
 // internal copies xs / ys and the epilogue gathers y (and the dot) back
+static int plan_product_(pars3_plan *pl, const double *x, double *y, bool acc, const double *w,
+                         double *dot, cudaStream_t st);
 static int plan_product(pars3_plan *pl, const double *x, double *y, bool acc, const double *w,
                         double *dot, cudaStream_t st) {
     if (pl->n > 0 && x == y) PARS3_FAIL(PARS3_ERR_ARG, "x and y must not alias");
+    pl->prof_k = 0;
+    mark(pl, st);
+    const int rc = plan_product_(pl, x, y, acc, w, dot, st);
+    while (pl->prof && pl->prof_k < 4) mark(pl, st);  // (phases a form does not have: empty)
+    return rc;
+}
+
+static int plan_product_(pars3_plan *pl, const double *x, double *y, bool acc, const double *w,
+                         double *dot, cudaStream_t st) {
     const bool grid = pl->grid_ok && !acc && pl->peers.nranks == 0 && pl->ntiles > 0;
     if (!pl->perm) {
         if (pl->direct) {
@@ -1803,6 +1824,43 @@ extern "C" int pars3_plan_spmv_dot(pars3_plan *pl, const double *x, double *y, c
                                    double *dot, void *stream) {
     if (!pl || !dot || (pl->n > 0 && (!x || !y || !w))) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
     return plan_product(pl, x, y, false, w, dot, (cudaStream_t)stream);
+}
+
+// Phase times of `reps` products y = A x (and <y, y> when with_dot), CUDA
+// events on `stream`: ms[0] the main kernel (tiles / full CSR; for a
+// locality plan with its gather of x), ms[1] the next phase (k_finish / the
+// span fix-up / the RED form's dot), ms[2] the rest (the gather of y, sums),
+// ms[3] the whole product; averages per product.
+extern "C" int pars3_plan_profile(pars3_plan *pl, const double *x, double *y, int32_t with_dot, int32_t reps,
+                                  double *ms, void *stream) {
+    if (!pl || !ms || reps < 1 || (pl->n > 0 && (!x || !y))) PARS3_FAIL(PARS3_ERR_ARG, "bad argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaEvent_t ev[4];
+    for (int k = 0; k < 4; k++) CUDA_TRY(cudaEventCreate(&ev[k]));
+    double *dot = nullptr;
+    if (with_dot) CUDA_TRY(cudaMalloc((void **)&dot, sizeof(double)));
+    double acc[4] = {0, 0, 0, 0};
+    int rc = PARS3_OK;
+    for (int r = 0; r < reps && rc == PARS3_OK; r++) {
+        pl->prof = ev;
+        rc = plan_product(pl, x, y, false, with_dot ? y : nullptr, dot, st);
+        pl->prof = nullptr;
+        if (rc) break;
+        if (cudaEventSynchronize(ev[3]) != cudaSuccess) { rc = PARS3_ERR_CUDA; break; }
+        float t[3];
+        for (int k = 0; k < 3; k++) cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]);
+        acc[0] += t[0];
+        acc[1] += t[1];
+        acc[2] += t[2];
+        acc[3] += t[0] + t[1] + t[2];
+    }
+    for (int k = 0; k < 4; k++) {
+        ms[k] = acc[k] / reps;
+        cudaEventDestroy(ev[k]);
+    }
+    if (dot) cudaFree(dot);
+    if (rc) PARS3_FAIL(rc, "pars3_plan_profile: product failed");
+    return PARS3_OK;
 }
 
 extern "C" int pars3_dot(int64_t n, const double *a, const double *b, double *out, void *stream) {

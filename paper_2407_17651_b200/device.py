@@ -166,6 +166,19 @@ class Pars3Operator:
                    "pars3_plan_status")
         return int(f.value)
 
+    def profile(self, x, y=None, with_dot=True, reps=20, stream=None) -> dict:
+        """Per-phase times of ``reps`` products (CUDA events on the stream):
+        the main kernel, the finish / fix-up phase, the rest, the total (ms
+        per product; pars3_plan_profile)."""
+        if y is None:
+            y = self.torch.empty(self.n, dtype=self.torch.float64, device=self.device)
+        ms = np.zeros(4)
+        _lib.check(self._L.pars3_plan_profile(self._handle, _lib.ptr(x), _lib.ptr(y), int(bool(with_dot)),
+                                              int(reps), _lib.ptr(ms), _lib.stream_ptr(stream)),
+                   "pars3_plan_profile")
+        return {"main_ms": float(ms[0]), "finish_ms": float(ms[1]), "rest_ms": float(ms[2]),
+                "total_ms": float(ms[3])}
+
     def kernel_count(self, with_dot: bool = False) -> int:
         c = ctypes.c_int32()
         _lib.check(self._L.pars3_plan_kernel_count(self._handle, int(with_dot), ctypes.byref(c)))
