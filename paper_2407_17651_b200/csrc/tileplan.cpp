@@ -219,8 +219,13 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
     make_windows(scratch, o.gap, true, R.n, d);
     cut_windows(o.cuts, d);
     // too fragmented for windows: the tile will carry an explicit column
-    // list, so do not pay for gap or alignment slots
-    if ((int)d.wlo.size() > kMaxWindows) make_windows(scratch, 0, false, R.n, d);
+    // list, so do not pay for gap or alignment slots (the rebuilt windows
+    // are cut again: a tile that ends up with <= kMaxWindows of them stays
+    // in window mode, and no window may straddle a rank boundary)
+    if ((int)d.wlo.size() > kMaxWindows) {
+        make_windows(scratch, 0, false, R.n, d);
+        cut_windows(o.cuts, d);
+    }
     if (d.local <= o.local_slots && !chunk_row) {
         out.push_back(std::move(d));
         return;
@@ -372,6 +377,19 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
         std::vector<Built> built(nt);
 #pragma omp parallel for schedule(dynamic, 4)
         for (int64_t t = 0; t < nt; t++) materialise(R, *flat[t], o, built[t]);
+        if (!o.cuts.empty()) {  // peer mode: a window's x and deliveries belong to one rank
+            bool straddle = false;
+#pragma omp parallel for reduction(|| : straddle)
+            for (int64_t t = 0; t < nt; t++) {
+                const Built &b = built[t];
+                if (b.list) continue;
+                for (size_t w = 0; w < b.wlo.size(); w++) {
+                    auto it = std::upper_bound(o.cuts.begin(), o.cuts.end(), b.wlo[w]);
+                    straddle = straddle || (it != o.cuts.end() && *it < b.wlo[w] + b.wlen[w]);
+                }
+            }
+            if (straddle) PARS3_FAIL(PARS3_ERR_STRUCT, "tile plan: a window straddles a block boundary");
+        }
 
         P = HostPlan();
         P.n = n;

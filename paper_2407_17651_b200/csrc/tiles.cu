@@ -47,6 +47,24 @@
 
 #include "common.h"
 #include "fullcsr.h"
+
+// PARS3_CHECKS builds (make checked -> libpars3_checked.so, selected with
+// PARS3_LIB): device-side bounds checks on every shared slot, row and column
+// index the kernels derive from the plan (a trap reports the failure)
+#ifdef PARS3_CHECKS
+#define DCHECK(cond)                                                                              \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("pars3 check failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,        \
+                   blockIdx.x, threadIdx.x, #cond);                                               \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define DCHECK(cond) \
+    do {             \
+    } while (0)
+#endif
 #include "locality.h"
 #include "tileplan.h"
 
@@ -144,6 +162,7 @@ struct DevPlan {
     const int32_t *ucol;
     const double *diag;
     int32_t ntiles;
+    int32_t n;  // rows (index space) of the plan
     int32_t watchdog;
     int32_t diag_const;  // 1: every diagonal value equals diag_alpha (strict / shifted skew)
     double diag_alpha;
@@ -395,6 +414,7 @@ __device__ __forceinline__ void stream_tile(const DevPlan &P, const int64_t *off
                 li[u] = __ldcs(ip + 32 * u);
             }
         }
+        DCHECK(rl <= kSink);
         const double xr = xs[rl];
         double c0 = 0.0, c1 = 0.0;  // two row-sum chains: even and odd slots
         if (kAcc > 0) {
@@ -402,6 +422,7 @@ __device__ __forceinline__ void stream_tile(const DevPlan &P, const int64_t *off
 #pragma unroll
             for (int u = 0; u < kMaxSlots; u++) {
                 if (u < ns) {
+                    DCHECK(li[u] <= kSink);
                     if (u & 1)
                         c1 = fma(v[u], xs[li[u]], c1);
                     else
@@ -682,6 +703,7 @@ __device__ __forceinline__ void tile_loop(const DevPlan &P, const double *__rest
                 if (c >= r0 && c < r1)
                     V += __double2ll_rn((P.diag_const ? P.diag_alpha : __ldg(P.diag + c)) * __ldg(x + c) *
                                         gscale);
+                DCHECK(c >= 0 && c < P.n);
                 if (V != 0) red_add_u64(P.yacc + c, V);
             };
             if (u0 >= 0) {
@@ -719,6 +741,7 @@ __device__ __forceinline__ void tile_loop(const DevPlan &P, const double *__rest
                     }
                     if (mine && c >= r0 && c < r1)  // (a halo row's diagonal belongs to its owner)
                         a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), __ldg(x + c), a);
+                    DCHECK(kPeer || (c >= 0 && c < P.n));
                     if (a != 0.0) atomicAdd(dst, a);
                 }
             } else {
@@ -740,6 +763,7 @@ __device__ __forceinline__ void tile_loop(const DevPlan &P, const double *__rest
                         double a = take(off + i);
                         if (mine && c >= r0 && c < r1)
                             a = fma(P.diag_const ? P.diag_alpha : __ldg(P.diag + c), __ldg(x + c), a);
+                        DCHECK(kPeer || (c >= 0 && c < P.n));
                         if (a != 0.0) atomicAdd(dst + i, a);
                     }
                 }
@@ -1050,7 +1074,8 @@ __global__ void __launch_bounds__(512) k_perm_out(int32_t n, const int32_t *__re
 // partials in warp order.  No atomics: every y element is written once, the
 // sum order is fixed by the plan (bitwise repeatable), and the arithmetic
 // is plain fp64 (IEEE semantics for non-finite inputs).
-__global__ void __launch_bounds__(256, 2) k_csr(int64_t ne, int64_t nwarps, const int32_t *__restrict__ col,
+__global__ void __launch_bounds__(256, 2) k_csr(int32_t nrows, int64_t ne, int64_t nwarps,
+                                                const int32_t *__restrict__ col,
                                                 const double *__restrict__ val,
                                                 const int32_t *__restrict__ lane_row,
                                                 const uint32_t *__restrict__ lane_flags,
@@ -1076,7 +1101,10 @@ __global__ void __launch_bounds__(256, 2) k_csr(int64_t ne, int64_t nwarps, cons
         const int32_t row0 = __ldcs(lane_row + L);
         const uint32_t fl = __ldcs(lane_flags + L);
 #pragma unroll
-        for (int k = 0; k < K; k++) xc[k] = e0 + k < ne ? __ldg(x + c[k]) : 0.0;  // all in flight
+        for (int k = 0; k < K; k++) {
+            DCHECK(e0 + k >= ne || (c[k] >= 0 && c[k] < nrows));
+            xc[k] = e0 + k < ne ? __ldg(x + c[k]) : 0.0;  // all in flight
+        }
 #pragma unroll
         for (int h = 0; h < K / 2; h++) {
             const double2 a = __ldcs(v2 + h);
@@ -1091,6 +1119,7 @@ __global__ void __launch_bounds__(256, 2) k_csr(int64_t ne, int64_t nwarps, cons
 #pragma unroll
         for (int k = 0; k < K; k++) {
             if (k > 0 && ((fl >> k) & 1u)) {
+                DCHECK(r >= 0 && r < nrows);
                 if (first && cont)
                     head = s;
                 else
@@ -1611,6 +1640,7 @@ static DevPlan dev_plan(const pars3_plan *pl) {
     P.ucol = pl->ucol;
     P.diag = pl->diag;
     P.ntiles = pl->ntiles;
+    P.n = (int32_t)pl->n;
     P.watchdog = pl->watchdog;
     P.diag_const = pl->diag_const;
     P.diag_alpha = pl->diag_alpha;
@@ -1698,7 +1728,7 @@ static int launch_direct(pars3_plan *pl, const double *x, double *y, bool acc, c
         out = pl->yacc_tmp;
     }
     const int grid = (int)std::min<int64_t>(148 * 2, (pl->nwarps + 7) / 8);
-    k_csr<<<grid, 256, 0, st>>>(pl->ne, pl->nwarps, pl->ccol, pl->cval, pl->clrow, pl->clflags, x, out,
+    k_csr<<<grid, 256, 0, st>>>((int32_t)pl->n, pl->ne, pl->nwarps, pl->ccol, pl->cval, pl->clrow, pl->clflags, x, out,
                                 pl->whead, pl->wtail);
     LAUNCH_CHECK();
     mark(pl, st);
