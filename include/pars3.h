@@ -154,6 +154,19 @@ int pars3_ipc_close(void *ptr);
  * spmv_pars3 parallel.py:136-183).  y is overwritten. */
 int pars3_plan_spmv(pars3_plan *plan, const double *x, double *y, void *stream);
 
+/* The general product entry: y = A x (or y += A x with PARS3_PRODUCT_ACC),
+ * with *dot = <y, w> when dot != NULL (w may equal y).  Single-GPU products
+ * are bitwise repeatable: their deliveries are exact integers on one
+ * fixed-point grid per product.  The grid's scale comes from the previous
+ * product's max |x| (a product whose x exceeds it is redone in fp64 on the
+ * device), so the bits of A x can depend on that history where a delivery
+ * is rounded to the grid; PARS3_PRODUCT_STRICT takes the scale from a pass
+ * over this x instead (a pure function of x; one extra read of x). */
+#define PARS3_PRODUCT_ACC 1
+#define PARS3_PRODUCT_STRICT 2
+int pars3_plan_product(pars3_plan *plan, const double *x, double *y, const double *w, double *dot,
+                       int32_t flags, void *stream);
+
 /* y += A x through a plan (y is NOT zeroed): several plans over the same
  * index space (e.g. a rank's interior and boundary rows, DistributedPars3)
  * accumulate into one y. */
@@ -227,6 +240,24 @@ int pars3_mrs_lanczos(int64_t n, const double *y, const double *v, double *w, do
 int pars3_mrs_update(int64_t n, double *u, double inv_gamma, const double *v, double *dm2,
                      const double *dm1, double r0, double r1, double inv_r2, double tau,
                      double *x, void *stream);
+
+/* Device-resident MRS step (no host round trip per iteration): the
+ * recurrence scalars live in a device state of *size doubles (layout:
+ * gamma, c1, s1, c2, s2, phi, beta, norm2, r0, r1, 1/r2, tau, 1/g, done,
+ * tol, alpha, pending, ...); a per-CTA scratch of *parts doubles.
+ * pars3_mrs_lanczos_dev: w <- y - alpha v + gamma w, state.norm2 = <w, w> on
+ *   this rank's rows (fixed-order sum; a distributed caller all-reduces
+ *   state[7] next);
+ * pars3_mrs_rotate_dev: iteration j's Givens step, resid[j] = |phi_j|,
+ *   convergence flags;
+ * pars3_mrs_update_dev: d <- (v - r0 dm2 - r1 dm1) / r2 into dm2, x += tau
+ *   d, u <- u / g.  Every kernel is a no-op once the state says done. */
+int pars3_mrs_state_size(int32_t *size, int32_t *parts);
+int pars3_mrs_lanczos_dev(int64_t n, const double *y, const double *v, double *w, const double *state,
+                          double *part, void *stream);
+int pars3_mrs_rotate_dev(double *state, double *resid, int32_t j, void *stream);
+int pars3_mrs_update_dev(int64_t n, double *u, const double *v, double *dm2, const double *dm1, double *x,
+                         const double *state, void *stream);
 
 /* --------------------------------------------- host-native preprocessing */
 

@@ -20,7 +20,7 @@ from .generate import generate_band_skew
 from .instrument import (AccumulationMessage, Pars3Trace, WorkerContext, spmv_pars3_instrumented,
                          spmv_serial_instrumented)
 from .mmio import ParseError, read_matrix, read_vector, write_matrix, write_vector
-from .mrs import MrsResult, mrs_solve
+from .mrs import MrsResult, mrs_solve, mrs_solve_distributed
 from .parallel import prepare, spmv_atomic, spmv_pars3
 from .reorder import (AdjacencyPattern, Permutation, apply_permutation, compute_bandwidth,
                       pattern_from_coo, pattern_from_sss, permute_sss, rcm_order, rcm_order_sss,

@@ -52,6 +52,8 @@ PLAN_LOCALITY = 8      # try the internal locality order on every plan (pars3.h)
 PLAN_NO_LOCALITY = 16  # never use it
 PLAN_DIRECT = 32       # direct mode (no shared staging) forced (pars3.h)
 PLAN_NO_DIRECT = 64    # never direct mode
+PRODUCT_ACC = 1        # pars3_plan_product: y += A x
+PRODUCT_STRICT = 2     # the grid scale from this x (a pure function of x)
 
 
 # name -> (restype, argtypes)
@@ -77,12 +79,17 @@ _SIGS = {
     "pars3_locality_order": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, ctypes.POINTER(_c_i64)]),
     "pars3_full_csr_host": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_plan_profile": (ctypes.c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _vp, _vp]),
+    "pars3_plan_product": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _c_i32, _vp]),
     "pars3_plan_status": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i32), _vp]),
     "pars3_plan_kernel_count": (ctypes.c_int, [_vp, _c_i32, ctypes.POINTER(_c_i32)]),
     "pars3_plan_destroy": (ctypes.c_int, [_vp]),
     "pars3_plan_phases": (ctypes.c_int, [_vp, _vp]),
     "pars3_mrs_lanczos": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, ctypes.c_double, ctypes.c_double,
                                          _vp, _vp]),
+    "pars3_mrs_state_size": (ctypes.c_int, [_vp, _vp]),
+    "pars3_mrs_lanczos_dev": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pars3_mrs_rotate_dev": (ctypes.c_int, [_vp, _vp, _c_i32, _vp]),
+    "pars3_mrs_update_dev": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_mrs_update": (ctypes.c_int, [_c_i64, _vp, ctypes.c_double, _vp, _vp, _vp,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_double, _vp, _vp]),

@@ -93,6 +93,7 @@ constexpr int kMaxSlots = 8;          // slots per slice (plan seg_max)
 constexpr int kMaxWindowsDev = pars3::kMaxWindows;
 constexpr int kLocalExact = PARS3_CAP;  // window slots per tile: x + fp64 acc or two words (16 B/slot)
 constexpr int kLocalFixed = PARS3_CAP == 3200 ? 2496 : PARS3_CAP * 4 / 5 / 32 * 32;  // x + 3 words (20 B/slot)
+static_assert(kThreads % 32 == 0 && kThreads <= 1024, "CTA shape");
 constexpr int kTerms2 = 64;        // two-word fixed point: max terms per slot per tile
 constexpr int kTerms3 = 4096;      // three-word fixed point: max terms per slot per tile
 // Shared arrays are laid out with a compile-time stride (so the second and
@@ -139,12 +140,13 @@ struct GState {
     int32_t flags;       // why the grid result must be redone (kFlag*), cleared by k_finish
     int32_t xe;          // grid scale bound |x| < 2^xe assumed by the next product
     int32_t xe_seen;     // max x exponent over this product's tiles
-    int32_t spare;
+    int32_t done;        // k_conv CTAs done
     uint32_t bar;        // grid barrier of k_finish: arrivals
     uint32_t gen;        // grid barrier of k_finish: generation
     int32_t fp64_tiles;  // tiles accumulated in fp64 (guard or non-finite x), cumulative
     int32_t redone;      // products redone by k_finish, cumulative
-    int32_t pad[6];
+    int32_t xe_pre;      // strict scale: max x exponent of THIS product's x + 1 + kXeBias (0: none)
+    int32_t pad[5];
 };
 constexpr int kFlagNonfinite = 1;  // a non-finite x value: IEEE semantics need the fp64 form
 constexpr int kFlagXRange = 2;     // some |x| >= 2^xe: the grid could overflow
@@ -153,6 +155,7 @@ constexpr int kFlagScale = 8;      // grid exponent outside the fp64 range
 constexpr int kFlagTileFp = 16;    // a tile the fixed point cannot carry (guard, scale range)
 constexpr int kXeNone = -1100;     // "no finite non-zero x seen"
 constexpr int kExNonfinite = 4000; // x exponent scan: a non-finite value
+constexpr int kXeBias = 2048;      // GState::xe_pre encoding (a memset to 0 means "none")
 
 struct DevPlan {
     const TileMeta *tiles;
@@ -181,6 +184,7 @@ struct DevPlan {
     int32_t ev_g;   // every |value| and |diag| < 2^ev_g
     int32_t hgrid;  // ceil(log2(most terms one y element sums))
     int32_t cmax;   // most tiles delivering to one row block (grid roundings per element)
+    int32_t strict; // this product's scale from its own x (k_xmax pre-pass), not the previous one's
 };
 
 
@@ -470,6 +474,16 @@ __device__ __forceinline__ double cta_max(double v, double *sred) {
     return v;
 }
 
+// The scale bound of this product's grid: strict products take it from a
+// pass over their own x (k_xmax, a pure function of x), the others from the
+// previous product's maximum (k_conv's update; bitwise the same when x
+// repeats, and checked by kFlagXRange when it grows).
+__device__ __forceinline__ int product_xe(const DevPlan &P) {
+    if (!P.strict) return *(volatile int32_t *)&P.gs->xe;
+    const int e = *(volatile int32_t *)&P.gs->xe_pre;
+    return e == 0 ? kXeNone : e - kXeBias;
+}
+
 // The persistent tile loop.  kWords: the plan's accumulator (0 fp64, 2 / 3
 // fixed-point words; fixed-point plans switch single tiles to fp64).
 // kPeer: multi-GPU peer mode (P.peers; RED form only).  kGrid: GRID form
@@ -513,7 +527,7 @@ __device__ __forceinline__ void tile_loop(const DevPlan &P, const double *__rest
     // the grid of this product: yacc unit 2^(Eg-62), |partial sums| < 2^(Eg+1)
     int Eg = 0, xe = 0;
     if (kGrid) {
-        xe = *(volatile int32_t *)&P.gs->xe;
+        xe = product_xe(P);
         Eg = P.ev_g + xe + P.hgrid;
         if (Eg > 960 || Eg < -960) {
             if (tid == 0) atomicOr(&P.gs->flags, kFlagScale);
@@ -807,6 +821,133 @@ __device__ __forceinline__ void grid_sync(GState *g) {
     __syncthreads();
 }
 
+// The grid product's finish, one streaming pass: y = yacc * 2^(Eg-62) with
+// yacc cleared for the next product, and per-CTA shares of <y, w> and
+// ||y||_inf (a fixed row assignment: the grid is fixed per plan); the CTA
+// that finishes last sums the shares in CTA order, runs the accuracy check
+// (the grid's rounding against ||y||_inf) and sets the next product's scale
+// bound.  No shared memory, many CTAs, eight pairs in flight per thread.
+constexpr int kConvThreads = 256;
+constexpr int kConvGrid = 148 * 8;
+__global__ void __launch_bounds__(kConvThreads) k_conv(DevPlan P, double *__restrict__ y, const double *w,
+                                                       double *dot, int dot_self, int32_t n) {
+    __shared__ double s_red[kConvThreads / 32];
+    __shared__ int s_last;
+    GState *g = P.gs;
+    const int xe = product_xe(P);
+    const int Eg = max(-960, min(960, P.ev_g + xe + P.hgrid));
+    const double gunit = ldexp(1.0, Eg - 62);
+    const bool self = dot_self != 0;
+    const int64_t stride = (int64_t)gridDim.x * kConvThreads;
+    const int64_t i0 = blockIdx.x * (int64_t)kConvThreads + threadIdx.x;
+    double d = 0.0, mx = 0.0;
+    if ((((uintptr_t)y | (uintptr_t)w) & 15) == 0) {  // pairs: 16-byte accesses
+        const int64_t n2 = n / 2;
+        longlong2 *a2 = reinterpret_cast<longlong2 *>(P.yacc);
+        double2 *y2 = reinterpret_cast<double2 *>(y);
+        const double2 *w2 = reinterpret_cast<const double2 *>(w);
+        constexpr int U = 8;
+        for (int64_t i = i0; i < n2; i += U * stride) {
+            longlong2 Y[U];
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (i + u * stride < n2) Y[u] = __ldcs(a2 + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int64_t j = i + u * stride;
+                if (j < n2) {
+                    __stcs(a2 + j, make_longlong2(0, 0));
+                    const double2 v = make_double2((double)Y[u].x * gunit, (double)Y[u].y * gunit);
+                    __stcs(y2 + j, v);
+                    if (dot) {
+                        const double2 q = self ? v : __ldcs(w2 + j);
+                        d = fma(v.y, q.y, fma(v.x, q.x, d));
+                    }
+                    mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+                }
+            }
+        }
+        if ((n & 1) && i0 == 0) {
+            const long long Y = P.yacc[n - 1];
+            P.yacc[n - 1] = 0;
+            const double v = (double)Y * gunit;
+            y[n - 1] = v;
+            if (dot) d = fma(v, self ? v : w[n - 1], d);
+            mx = fmax(mx, fabs(v));
+        }
+    } else {
+        for (int64_t i = i0; i < n; i += stride) {
+            const long long Y = P.yacc[i];
+            P.yacc[i] = 0;
+            const double v = (double)Y * gunit;
+            y[i] = v;
+            if (dot) d = fma(v, self ? v : w[i], d);
+            mx = fmax(mx, fabs(v));
+        }
+    }
+    // fixed-tree CTA sums (cta_sum's shape with this CTA size)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 16; o; o >>= 1) {
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) s_red[warp] = d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int k = 0; k < kConvThreads / 32; k++) s += s_red[k];
+        P.blk_dot[blockIdx.x] = s;
+    }
+    __syncthreads();
+    if (lane == 0) s_red[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int k = 0; k < kConvThreads / 32; k++) m = fmax(m, s_red[k]);
+        P.blk_max[blockIdx.x] = m;
+        __threadfence();
+        s_last = atomicAdd(&g->done, 1) == (int)gridDim.x - 1;
+        if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (!s_last) return;
+    d = 0.0;
+    mx = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kConvThreads) {  // CTA order per thread
+        d += __ldcg(P.blk_dot + b);
+        mx = fmax(mx, __ldcg(P.blk_max + b));
+    }
+    for (int o = 16; o; o >>= 1) {
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    __syncthreads();
+    if (lane == 0) s_red[warp] = d;
+    __syncthreads();
+    double dsum = 0.0;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < kConvThreads / 32; k++) dsum += s_red[k];
+    __syncthreads();
+    if (lane == 0) s_red[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int k = 0; k < kConvThreads / 32; k++) m = fmax(m, s_red[k]);
+        if (dot) *dot = dsum;
+        // each delivery was rounded to the grid unit 2^(Eg-62) once: the
+        // grid's share of the error stays below 2^-44 max(1, ||y||_inf),
+        // else k_finish redoes the product (a matrix whose value range the x
+        // correlate with)
+        const double err = (double)P.cmax * ldexp(1.0, Eg - 63);
+        if (!(err <= ldexp(1.0, -44) * fmax(1.0, m))) atomicOr(&g->flags, kFlagCoarse);
+        const int xs = *(volatile int32_t *)&g->xe_seen;
+        g->xe = (xs <= kXeNone ? -1000 : xs) + 1;
+        g->xe_seen = kXeNone;
+        g->done = 0;
+        __threadfence();
+    }
+}
+
 // After every grid product (launched cooperatively: every CTA resident).
 // It first finishes the product in one streaming pass: y = yacc * 2^(Eg-62), yacc cleared, the
 // per-CTA shares of <y, w> and ||y||_inf (fixed row assignment), summed in
@@ -825,87 +966,6 @@ k_finish(DevPlan P, const double *__restrict__ x, double *__restrict__ y, const 
     __shared__ double s_red[kWarps];
     const int64_t stride = (int64_t)gridDim.x * kThreads;
     const int64_t i0 = blockIdx.x * (int64_t)kThreads + threadIdx.x;
-    {
-        const int xe = *(volatile int32_t *)&g->xe;
-        const int Eg = max(-960, min(960, P.ev_g + xe + P.hgrid));
-        const double gunit = ldexp(1.0, Eg - 62);
-        double d = 0.0, mx = 0.0;
-        const bool self = dot_self != 0;
-        if ((((uintptr_t)y | (uintptr_t)w) & 15) == 0) {  // pairs: 16-byte accesses
-            const int64_t n2 = n / 2;
-            longlong2 *a2 = reinterpret_cast<longlong2 *>(P.yacc);
-            double2 *y2 = reinterpret_cast<double2 *>(y);
-            const double2 *w2 = reinterpret_cast<const double2 *>(w);
-            for (int64_t i = i0; i < n2; i += 4 * stride) {  // four pairs in flight per thread
-                longlong2 Y[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++)
-                    if (i + u * stride < n2) Y[u] = __ldcs(a2 + i + u * stride);
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int64_t j = i + u * stride;
-                    if (j < n2) {
-                        __stcs(a2 + j, make_longlong2(0, 0));
-                        const double2 v = make_double2((double)Y[u].x * gunit, (double)Y[u].y * gunit);
-                        __stcs(y2 + j, v);
-                        if (dot) {
-                            const double2 q = self ? v : __ldcs(w2 + j);
-                            d = fma(v.y, q.y, fma(v.x, q.x, d));
-                        }
-                        mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
-                    }
-                }
-            }
-            if ((n & 1) && i0 == 0) {
-                const long long Y = P.yacc[n - 1];
-                P.yacc[n - 1] = 0;
-                const double v = (double)Y * gunit;
-                y[n - 1] = v;
-                if (dot) d = fma(v, self ? v : w[n - 1], d);
-                mx = fmax(mx, fabs(v));
-            }
-        } else {
-            for (int64_t i = i0; i < n; i += stride) {
-                const long long Y = P.yacc[i];
-                P.yacc[i] = 0;
-                const double v = (double)Y * gunit;
-                y[i] = v;
-                if (dot) d = fma(v, self ? v : w[i], d);
-                mx = fmax(mx, fabs(v));
-            }
-        }
-        d = cta_sum(d, s_red);
-        mx = cta_max(mx, s_red);
-        if (threadIdx.x == 0) {
-            P.blk_dot[blockIdx.x] = d;
-            P.blk_max[blockIdx.x] = mx;
-        }
-        grid_sync(g);
-        if (blockIdx.x == 0) {
-            d = 0.0;
-            mx = 0.0;
-            for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) {
-                d += __ldcg(P.blk_dot + b);
-                mx = fmax(mx, __ldcg(P.blk_max + b));
-            }
-            d = cta_sum(d, s_red);
-            mx = cta_max(mx, s_red);
-            if (threadIdx.x == 0) {
-                if (dot) *dot = d;
-                // each delivery was rounded to the grid unit 2^(Eg-62) once:
-                // the grid's share of the error stays below 2^-44
-                // max(1, ||y||_inf), else the fp64 pass redoes the product
-                // (a matrix whose value range the x correlate with)
-                const double err = (double)P.cmax * ldexp(1.0, Eg - 63);
-                if (!(err <= ldexp(1.0, -44) * fmax(1.0, mx))) atomicOr(&g->flags, kFlagCoarse);
-                const int xs = *(volatile int32_t *)&g->xe_seen;
-                g->xe = (xs <= kXeNone ? -1000 : xs) + 1;
-                g->xe_seen = kXeNone;
-                __threadfence();
-            }
-        }
-        grid_sync(g);
-    }
     if (__ldcg(&g->flags) == 0) {
         if (blockIdx.x == 0 && threadIdx.x == 0) g->claim = 0;
         return;
@@ -940,8 +1000,8 @@ k_finish(DevPlan P, const double *__restrict__ x, double *__restrict__ y, const 
     }
 }
 
-// max binary exponent of x (|x| < 2^e) into gs->xe: the first grid product's
-// scale bound (later products use the previous one's maximum)
+// max binary exponent of x (|x| < 2^e) + 1 into gs->xe_pre (biased; zeroed
+// before): a strict product's scale bound (the first product is strict)
 __global__ void __launch_bounds__(512) k_xmax(int32_t n, const double *__restrict__ x, GState *g) {
     int e = kXeNone;
     const int32_t stride = gridDim.x * blockDim.x;
@@ -950,7 +1010,7 @@ __global__ void __launch_bounds__(512) k_xmax(int32_t n, const double *__restric
         if (b != 2047) e = max(e, max(b, 1) - 1022);
     }
     e = __reduce_max_sync(0xffffffffu, e);
-    if ((threadIdx.x & 31) == 0 && e > kXeNone) atomicMax(&g->xe, e + 1);
+    if ((threadIdx.x & 31) == 0 && e > kXeNone) atomicMax(&g->xe_pre, e + 1 + kXeBias);
 }
 
 // <a, b>: 16-byte loads, four in flight per thread; each block writes its
@@ -1351,6 +1411,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     if (p < 1) PARS3_FAIL(PARS3_ERR_ARG, "worker count must be at least 1, got %d", p);
     PlanOptions o0;
     int32_t max_ctas = 0, flags = 0;
+    if (const char *tr = getenv("PARS3_TILE_ROWS")) o0.tile_rows = std::max(1, atoi(tr));  // tuning knob
     if (opt) {
         if (opt->tile_rows > 0) o0.tile_rows = opt->tile_rows;
         if (opt->local_slots > 0) o0.local_slots = opt->local_slots;
@@ -1573,6 +1634,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     }
     ZALLOC(gs, 1);
     ZALLOC(part, kDotGrid);
+    static_assert(kConvGrid >= kDotGrid, "blk_dot / blk_max hold k_conv's shares");
     {
         GState g0{};
         g0.xe = kXeNone;
@@ -1586,8 +1648,8 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         pl->ev_g = G.ev_g;
         pl->hgrid = G.hgrid;
         pl->cmax = G.cmax;
-        ZALLOC(blk_dot, std::max<int64_t>(pl->ntiles, kDotGrid));
-        ZALLOC(blk_max, std::max<int64_t>(pl->ntiles, kDotGrid));
+        ZALLOC(blk_dot, std::max<int64_t>(pl->ntiles, kConvGrid));
+        ZALLOC(blk_max, std::max<int64_t>(pl->ntiles, kConvGrid));
         ZALLOC(yacc, pl->n);
     }
 #undef UP
@@ -1690,14 +1752,16 @@ static int launch_red(pars3_plan *pl, const double *x, double *y, bool acc, cuda
 // GRID form: y = A x written by the block finalizers, *dot = <y, w> fused
 // when w is y (dot_self) or given, by k_finish (which redoes flagged products)
 static int launch_grid(pars3_plan *pl, const double *x, double *y, const double *w, double *dot,
-                       bool dot_self, cudaStream_t st) {
-    if (!pl->xe_ready) {  // first product: the scale bound from a pass over x
+                       bool dot_self, bool strict, cudaStream_t st) {
+    DevPlan P = dev_plan(pl);
+    if (strict || !pl->xe_ready) {  // the scale bound from a pass over this x
+        CUDA_TRY(cudaMemsetAsync(&pl->gs->xe_pre, 0, sizeof(int32_t), st));
         const int grid = (int)std::min<int64_t>(148 * 4, (pl->n + 511) / 512);
         k_xmax<<<grid, 512, 0, st>>>((int32_t)pl->n, x, pl->gs);
         LAUNCH_CHECK();
         pl->xe_ready = 1;
+        P.strict = 1;
     }
-    const DevPlan P = dev_plan(pl);
     const int ds = dot_self ? 1 : 0;
     if (pl->words == 0)
         k_tiles<0, false, true><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, w, dot, ds);
@@ -1708,6 +1772,8 @@ static int launch_grid(pars3_plan *pl, const double *x, double *y, const double 
     LAUNCH_CHECK();
     mark(pl, st);
     int32_t n32 = (int32_t)pl->n;
+    k_conv<<<kConvGrid, kConvThreads, 0, st>>>(P, y, w, dot, ds, n32);
+    LAUNCH_CHECK();
     void *args[] = {(void *)&P, (void *)&x, (void *)&y, (void *)&w, (void *)&dot, (void *)&ds, (void *)&n32};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_finish, dim3(pl->grid_redo), dim3(kThreads), args,
                                          kFinishSmem, st));
@@ -1792,19 +1858,19 @@ extern "C" int pars3_plan_set_peers(pars3_plan *pl, int32_t nranks, int32_t me, 
 // one product through the plan; with a locality order the tiles run on the
 // internal copies xs / ys and the epilogue gathers y (and the dot) back
 static int plan_product_(pars3_plan *pl, const double *x, double *y, bool acc, const double *w,
-                         double *dot, cudaStream_t st);
+                         double *dot, bool strict, cudaStream_t st);
 static int plan_product(pars3_plan *pl, const double *x, double *y, bool acc, const double *w,
-                        double *dot, cudaStream_t st) {
+                        double *dot, cudaStream_t st, bool strict = false) {
     if (pl->n > 0 && x == y) PARS3_FAIL(PARS3_ERR_ARG, "x and y must not alias");
     pl->prof_k = 0;
     mark(pl, st);
-    const int rc = plan_product_(pl, x, y, acc, w, dot, st);
+    const int rc = plan_product_(pl, x, y, acc, w, dot, strict, st);
     while (pl->prof && pl->prof_k < 4) mark(pl, st);  // (phases a form does not have: empty)
     return rc;
 }
 
 static int plan_product_(pars3_plan *pl, const double *x, double *y, bool acc, const double *w,
-                         double *dot, cudaStream_t st) {
+                         double *dot, bool strict, cudaStream_t st) {
     const bool grid = pl->grid_ok && !acc && pl->peers.nranks == 0 && pl->ntiles > 0;
     if (!pl->perm) {
         if (pl->direct) {
@@ -1812,7 +1878,7 @@ static int plan_product_(pars3_plan *pl, const double *x, double *y, bool acc, c
             if (rc || !dot) return rc;
             return launch_dot(pl->n, y, w, pl->part, dot, st);
         }
-        if (grid) return launch_grid(pl, x, y, w, dot, dot && w == y, st);
+        if (grid) return launch_grid(pl, x, y, w, dot, dot && w == y, strict, st);
         int rc = launch_red(pl, x, y, acc, st);
         if (rc || !dot) return rc;
         return launch_dot(pl->n, y, w, pl->part, dot, st);
@@ -1824,7 +1890,8 @@ static int plan_product_(pars3_plan *pl, const double *x, double *y, bool acc, c
     // <y, y> = <ys, ys>: fused into the grid pass; another w goes through
     // the gather's epilogue
     const bool fused = grid && dot && w == y;
-    int rc = grid ? launch_grid(pl, pl->xs, pl->ys, fused ? pl->ys : nullptr, fused ? dot : nullptr, fused, st)
+    int rc = grid ? launch_grid(pl, pl->xs, pl->ys, fused ? pl->ys : nullptr, fused ? dot : nullptr, fused,
+                                strict, st)
                   : launch_red(pl, pl->xs, pl->ys, false, st);
     if (rc) return rc;
     const bool pdot = dot && !fused;
@@ -1838,6 +1905,16 @@ static int plan_product_(pars3_plan *pl, const double *x, double *y, bool acc, c
         LAUNCH_CHECK();
     }
     return PARS3_OK;
+}
+
+// the general entry: flags PARS3_PRODUCT_ACC (y += A x), PARS3_PRODUCT_STRICT
+// (the grid scale from this x: a pure function of x), dot / w optional
+extern "C" int pars3_plan_product(pars3_plan *pl, const double *x, double *y, const double *w, double *dot,
+                                  int32_t flags, void *stream) {
+    if (!pl || (pl->n > 0 && (!x || !y)) || (dot && pl->n > 0 && !w)) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
+    if ((flags & PARS3_PRODUCT_ACC) && dot) PARS3_FAIL(PARS3_ERR_ARG, "y += A x has no fused dot");
+    return plan_product(pl, x, y, (flags & PARS3_PRODUCT_ACC) != 0, w, dot, (cudaStream_t)stream,
+                        (flags & PARS3_PRODUCT_STRICT) != 0);
 }
 
 extern "C" int pars3_plan_spmv(pars3_plan *pl, const double *x, double *y, void *stream) {
@@ -1926,9 +2003,9 @@ extern "C" int pars3_plan_kernel_count(const pars3_plan *pl, int32_t with_dot, i
     if (pl->direct) {
         c = (pl->n > 0 ? 1 : 0) + (pl->nspan > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 2 : 0);
     } else if (pl->perm) {
-        c = 2 + (pl->ntiles > 0 ? (grid ? 2 : 1) : 0);
+        c = 2 + (pl->ntiles > 0 ? (grid ? 3 : 1) : 0);
     } else if (grid) {
-        c = 2;
+        c = 3;  // k_tiles, k_conv, k_finish (exits at once unless the product was flagged)
     } else {
         c = (pl->ntiles > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 2 : 0);
     }

@@ -69,19 +69,22 @@ class Pars3Operator:
         self._L = L
 
     # -- hot entry points (device tensors in, device tensors out) ---------
-    def matvec(self, x, y=None, stream=None, accumulate=False):
+    def matvec(self, x, y=None, stream=None, accumulate=False, strict=False):
         """y = A x for a contiguous float64 CUDA tensor x of length n
-        (``accumulate``: y += A x, y not zeroed)."""
+        (``accumulate``: y += A x, y not zeroed).  ``strict``: the product's
+        fixed-point grid takes its scale from this x (a pure function of x,
+        one extra read of x) rather than from the previous product's
+        (pars3_plan_product, include/pars3.h)."""
         if y is None:
             y = self.torch.empty(self.n, dtype=self.torch.float64, device=self.device)
             if accumulate:
                 y.zero_()
-        f = self._L.pars3_plan_spmv_acc if accumulate else self._L.pars3_plan_spmv
-        _lib.check(f(self._handle, _lib.ptr(x), _lib.ptr(y), _lib.stream_ptr(stream)),
-                   "pars3_plan_spmv")
+        flags = (_lib.PRODUCT_ACC if accumulate else 0) | (_lib.PRODUCT_STRICT if strict else 0)
+        _lib.check(self._L.pars3_plan_product(self._handle, _lib.ptr(x), _lib.ptr(y), None, None, flags,
+                                              _lib.stream_ptr(stream)), "pars3_plan_product")
         return y
 
-    def matvec_dot(self, x, w, y=None, dot=None, stream=None):
+    def matvec_dot(self, x, w, y=None, dot=None, stream=None, strict=False):
         """y = A x and dot = <y, w> (device scalar tensor); ``w`` may be ``y``."""
         t = self.torch
         if y is None:
@@ -90,13 +93,13 @@ class Pars3Operator:
             w = y
         if dot is None:
             dot = t.empty(1, dtype=t.float64, device=self.device)
-        _lib.check(self._L.pars3_plan_spmv_dot(self._handle, _lib.ptr(x), _lib.ptr(y),
-                                               _lib.ptr(w), _lib.ptr(dot),
-                                               _lib.stream_ptr(stream)), "pars3_plan_spmv_dot")
+        _lib.check(self._L.pars3_plan_product(self._handle, _lib.ptr(x), _lib.ptr(y), _lib.ptr(w),
+                                              _lib.ptr(dot), _lib.PRODUCT_STRICT if strict else 0,
+                                              _lib.stream_ptr(stream)), "pars3_plan_product")
         return y, dot
 
     # -- host-resident vectors: pipelined copies --------------------------
-    def matvec_host(self, x, out=None, non_blocking=False):
+    def matvec_host(self, x, out=None, non_blocking=False, strict=True):
         """y = A x for a HOST float64 tensor x (pinned for overlap), result in
         the host tensor ``out``.  Three streams and double-buffered device
         vectors pipeline consecutive calls: call k+1's host->device copy runs
@@ -131,7 +134,7 @@ class Pars3Operator:
         pl["ev_x"][b].record(h2d)
         comp.wait_event(pl["ev_x"][b])
         comp.wait_event(pl["ev_out"][b])
-        self.matvec(pl["x"][b], pl["y"][b], stream=comp)
+        self.matvec(pl["x"][b], pl["y"][b], stream=comp, strict=strict)
         pl["ev_y"][b].record(comp)
         d2h.wait_event(pl["ev_y"][b])
         with torch.cuda.stream(d2h):

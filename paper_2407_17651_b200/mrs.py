@@ -11,9 +11,15 @@ solved by Givens rotations exactly as in MINRES, with the solution updated
 through three-term direction vectors.  The product computes A v (with the
 alpha diagonal), so the Lanczos vector is u = A v_j - alpha v_j + g_j v_{j-1}.
 
-Per iteration on the GPU: the tile kernel (y = A v_j), one fused pass for u
-and ||u||^2, one fused pass for v_{j+1}, the direction and x; the rotation
-scalars are a few flops on the host (one 8-byte read per iteration).
+Per iteration on the GPU, with no host round trip: the product (y = A v_j,
+the grid-form PARS3 kernels), one fused pass for u and its share of
+||u||^2, the fixed-order norm, the Givens rotation (one device thread: the
+recurrence scalars live in a device state), and one fused pass for the
+direction, x and v_{j+1}.  The host only swaps buffer handles; it reads the
+state every ``check_every`` iterations to stop early.  Distributed (one
+rank per GPU, rows sharded by partition_rows): each rank runs the same loop
+on its block with its distributed operator, and the norm is one 8-byte
+all-reduce per iteration on the device (NCCL), the rotation replicated.
 """
 
 from __future__ import annotations
@@ -21,9 +27,13 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import ctypes
+
+import numpy as np
+
 from . import _lib
 
-__all__ = ["MrsResult", "mrs_solve"]
+__all__ = ["MrsResult", "mrs_solve", "mrs_solve_distributed", "RankOperator"]
 
 
 @dataclass
@@ -34,10 +44,13 @@ class MrsResult:
     converged: bool = False
 
 
-def mrs_solve(op, b, alpha: float, tol: float = 1e-10, maxiter: int = 100, stream=None) -> MrsResult:
+def mrs_solve(op, b, alpha: float, tol: float = 1e-10, maxiter: int = 100, stream=None,
+              check_every: int = 10, group=None) -> MrsResult:
     """Solve (alpha I + S) x = b with the PARS3 operator ``op`` (whose matrix
     must be alpha*I + S) from x_0 = 0.  Stops when ||r_j|| <= tol * ||b|| or
-    after ``maxiter`` iterations."""
+    after ``maxiter`` iterations.  ``group``: a torch.distributed process
+    group when ``op`` is one rank's distributed operator and ``b`` that
+    rank's rows (the norms are then all-reduced on the device)."""
     import torch
     L = _lib.load()
     n = op.n
@@ -45,48 +58,84 @@ def mrs_solve(op, b, alpha: float, tol: float = 1e-10, maxiter: int = 100, strea
     t = torch.float64
     b = torch.as_tensor(b, dtype=t).to(dev).contiguous()
     st = _lib.stream_ptr(stream)
+    size, parts = ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(L.pars3_mrs_state_size(ctypes.byref(size), ctypes.byref(parts)))
+    state = torch.zeros(size.value, dtype=t, device=dev)
+    part = torch.zeros(parts.value, dtype=t, device=dev)
+    resid = torch.zeros(maxiter + 1, dtype=t, device=dev)
+
+    def allreduce(view):
+        if group is not None:
+            import torch.distributed as dist
+            dist.all_reduce(view, group=group)
+
+    bb = torch.dot(b, b).reshape(1)
+    allreduce(bb)
+    beta_t = torch.sqrt(bb)
+    # state: c1 = c2 = 1, phi = beta, beta, tol, alpha (device ops, no sync)
+    state[1] = 1.0
+    state[3] = 1.0
+    state[5:7] = beta_t.expand(2)
+    state[14] = float(tol)
+    state[15] = float(alpha)
+    resid[0:1] = beta_t
     x = torch.zeros(n, dtype=t, device=dev)
-    beta = float(torch.linalg.vector_norm(b).item())
-    res = MrsResult(x=x, iterations=0, residuals=[beta], converged=beta == 0.0)
-    if beta == 0.0:
-        return res
-    v = b / beta                       # v_j
+    v = b / torch.where(beta_t > 0, beta_t, torch.ones_like(beta_t))  # v_j
     w = torch.zeros(n, dtype=t, device=dev)   # v_{j-1}, then u
     dm1 = torch.zeros(n, dtype=t, device=dev)  # d_{j-1}
     dm2 = torch.zeros(n, dtype=t, device=dev)  # d_{j-2}, then d_j
     y = torch.empty(n, dtype=t, device=dev)
-    norm2 = torch.zeros(1, dtype=t, device=dev)
-    gamma = 0.0                        # g_j
-    c1, s1, c2, s2 = 1.0, 0.0, 1.0, 0.0  # rotations G_{j-1}, G_{j-2}
-    phi = beta
+    res = MrsResult(x=x, iterations=0)
+    if float(beta_t.item()) == 0.0:
+        res.residuals, res.converged = [0.0], True
+        return res
+    j = 0
     for j in range(1, maxiter + 1):
-        op.matvec(v, y, stream=stream)
-        _lib.check(L.pars3_mrs_lanczos(n, _lib.ptr(y), _lib.ptr(v), _lib.ptr(w), float(alpha),
-                                       float(gamma), _lib.ptr(norm2), st), "mrs_lanczos")
-        gnext = math.sqrt(float(norm2.item()))  # the step's inner product
-        # column j of H: (-g_j, alpha, g_{j+1}); previous rotations, then a new one
-        h1 = -gamma
-        r0 = s2 * h1
-        h1p = c2 * h1
-        r1 = c1 * h1p + s1 * alpha
-        h2p = -s1 * h1p + c1 * alpha
-        r2 = math.hypot(h2p, gnext)
-        c, s = (h2p / r2, gnext / r2) if r2 > 0 else (1.0, 0.0)
-        tau = c * phi
-        phi = -s * phi
-        inv_g = 1.0 / gnext if gnext > 0 else 0.0
-        _lib.check(L.pars3_mrs_update(n, _lib.ptr(w), inv_g, _lib.ptr(v), _lib.ptr(dm2),
-                                      _lib.ptr(dm1), r0, r1, 1.0 / r2, tau, _lib.ptr(x), st),
-                   "mrs_update")
+        op.matvec(v, y, stream=stream, strict=True)  # each product a pure function of v
+        _lib.check(L.pars3_mrs_lanczos_dev(n, _lib.ptr(y), _lib.ptr(v), _lib.ptr(w), _lib.ptr(state),
+                                           _lib.ptr(part), st), "mrs_lanczos")
+        allreduce(state[7:8])  # the step's inner product, summed over ranks
+        _lib.check(L.pars3_mrs_rotate_dev(_lib.ptr(state), _lib.ptr(resid), j, st), "mrs_rotate")
+        _lib.check(L.pars3_mrs_update_dev(n, _lib.ptr(w), _lib.ptr(v), _lib.ptr(dm2), _lib.ptr(dm1),
+                                          _lib.ptr(x), _lib.ptr(state), st), "mrs_update")
         # rotate the buffers: v_{j+1} <- w, v_j -> w's slot; d_j <- dm2
         v, w = w, v
         dm1, dm2 = dm2, dm1
-        gamma = gnext
-        c2, s2, c1, s1 = c1, s1, c, s
-        res.iterations = j
-        res.residuals.append(abs(phi))
-        if abs(phi) <= tol * beta or gnext == 0.0:
-            res.converged = True
+        if check_every and j % check_every == 0 and float(state[16].item()) != 0.0:
             break
+    flags = state[13:18].cpu().numpy()  # done, tol, alpha, pending, converged iteration
+    res.converged = bool(flags[3] != 0.0)
+    res.iterations = int(flags[4]) if res.converged else j
+    res.residuals = [float(r) for r in resid[:res.iterations + 1].cpu().numpy()]
     res.x = x
     return res
+
+
+class RankOperator:
+    """A distributed operator (PeerPars3 / DistributedPars3: one rank's rows)
+    seen through the single-GPU interface mrs_solve drives: ``n`` rows,
+    ``device``, ``matvec(v, y)``."""
+
+    def __init__(self, dop):
+        self.dop = dop
+        self.n = int(dop.shard.hi - dop.shard.lo)
+        self.device = dop.device
+
+    def matvec(self, v, y, stream=None, strict=True):
+        y.copy_(self.dop.matvec(v))
+        return y
+
+
+def mrs_solve_distributed(dop, b_own, alpha: float, group=None, tol: float = 1e-10, maxiter: int = 100,
+                          check_every: int = 10) -> MrsResult:
+    """MRS over ranks (one per GPU): each rank iterates on its row block
+    (``b_own`` = b[lo:hi]) with its distributed operator; the only exchange
+    besides the products is one 8-byte all-reduce per iteration (the norm),
+    on the device.  ``x`` of the result is this rank's block."""
+    return mrs_solve(RankOperator(dop), b_own, alpha, tol=tol, maxiter=maxiter, check_every=check_every,
+                     group=group if group is not None else _default_group())
+
+
+def _default_group():
+    import torch.distributed as dist
+    return dist.group.WORLD

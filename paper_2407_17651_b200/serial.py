@@ -34,12 +34,13 @@ def count_ops(m: SssMatrix) -> OpCounter:
     return OpCounter(element_reads=m.nnz_offdiag + m.n, multiply_adds=2 * m.nnz_offdiag + m.n)
 
 
-def _run(op, x, n, out=None, non_blocking=False):
+def _run(op, x, n, out=None, non_blocking=False, strict=True):
     """Dispatch on the input's home: CUDA tensor -> CUDA result; host torch
     tensor (pinned for async copies) -> host tensor (into ``out`` if given),
     through the operator's copy pipeline (``non_blocking``: consecutive calls
     overlap their copies; the result is ready after torch.cuda.synchronize());
-    anything else -> numpy."""
+    anything else -> numpy.  These one-call entry points are strict: the
+    product is a pure function of x, bit for bit (pars3_plan_product)."""
     from .device import require_cuda
     torch = require_cuda()
     if isinstance(x, torch.Tensor):
@@ -48,14 +49,14 @@ def _run(op, x, n, out=None, non_blocking=False):
         if not x.is_cuda:
             if x.dtype != torch.float64:
                 x = x.to(torch.float64)
-            return op.matvec_host(x.contiguous(), out, non_blocking=non_blocking)
+            return op.matvec_host(x.contiguous(), out, non_blocking=non_blocking, strict=strict)
         xd = x.to(device=op.device, dtype=torch.float64).contiguous()
-        return op.matvec(xd, out)
+        return op.matvec(xd, out, strict=strict)
     xv = as_vector(x, n)
     if n == 0:
         return np.zeros(0)
     xd = torch.from_numpy(xv).to(op.device)
-    return op.matvec(xd).cpu().numpy()
+    return op.matvec(xd, strict=strict).cpu().numpy()
 
 
 def spmv_serial(m: SssMatrix, x, out=None, non_blocking=False):

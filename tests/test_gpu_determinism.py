@@ -91,3 +91,29 @@ def test_scale_bound_follows_x(oracle):
         st = op.status()
         if redo is not None:
             assert bool(st & 1) == redo, (factor, st)
+
+
+def test_strict_products_are_pure(oracle):
+    """PARS3_PRODUCT_STRICT: the grid scale comes from this x, so A x is a
+    pure function of x bit for bit, whatever product ran before (the
+    adaptive default is bitwise repeatable for repeated x); the one-call
+    entry points (numpy, host tensors) are strict."""
+    import torch
+    from paper_2407_17651_b200 import generators as G
+    from paper_2407_17651_b200.device import operator_for_sss
+    g = G.random_band(20000, 500, 8, 0.02, seed_struct=1, seed_perm=2, seed_val=3)
+    m = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
+    op = operator_for_sss(m, options=(0, 0, 0, -1, 0, 16, 0))  # tiles, no locality order
+    x1 = torch.from_numpy(G.make_x(m.n, 1)).cuda()
+    decay = torch.from_numpy(np.exp(-np.linspace(0, 40, m.n))).cuda()  # scales spanning 2^-58 .. 1
+    ya = op.matvec(x1, strict=True).clone()
+    for other in (x1 * 1e5, x1 * decay, x1 * 3e-7):
+        op.matvec(other)
+        yb = op.matvec(x1, strict=True)
+        assert torch.equal(ya, yb)
+    # the one-call entry point (its own cached plan): strict as well
+    y_np = P.spmv_serial(m, x1.cpu().numpy())
+    P.spmv_serial(m, (x1 * 1e5).cpu().numpy())
+    assert np.array_equal(y_np, P.spmv_serial(m, x1.cpu().numpy()))
+    y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x1.cpu().numpy())
+    assert rel_err(y_np, y_ref) <= 1e-12

@@ -429,9 +429,10 @@ def test_locality_order(flags, oracle):
         assert abs(float(dot.item()) - float(yh @ yh)) <= 1e-12 * float(yh @ yh)
         _, dot2 = op.matvec_dot(xd, xd)
         assert abs(float(dot2.item()) - float(x @ yh)) <= 1e-12 * float(np.abs(x) @ np.abs(yh))
-        # grid form: tiles + k_finish; + perm in/out with a locality order;
-        # direct mode: init + direct + dot (two kernels)
-        assert op.kernel_count(True) == (4 if st["locality_order"] or st["direct"] else 2), st
+        # grid form: tiles + k_conv + k_finish; + perm in/out with a locality
+        # order; row-major form: full CSR + span fix-up + dot (two kernels)
+        expect = 5 if st["locality_order"] else 4 if st["direct"] else 3
+        assert op.kernel_count(True) == expect, st
 
 
 @pytest.mark.parametrize("flags", [0, 32, 64])
