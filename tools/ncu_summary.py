@@ -39,11 +39,22 @@ for r in rows[2:]:
                                       sorted(st.items(), key=lambda kv: -kv[1]) if v / tot > 0.01))
     break
 src = page("--page", "source", "--print-source", "sass")
-if len(src) > 2:
-    hh = src[1]
+# one section per captured kernel: a "Kernel Name" row, a header row, the SASS rows
+sect, cur = [], None
+for r in src:
+    if r and r[0] == "Kernel Name":
+        cur = {"name": r[1] if len(r) > 1 else "", "rows": []}
+        sect.append(cur)
+    elif cur is not None:
+        cur["rows"].append(r)
+for sc in sect:
+    if kname not in sc["name"] or len(sc["rows"]) < 2:
+        continue
+    hh = sc["rows"][0]
     i = hh.index("Warp Stall Sampling (All Samples)")
-    data = src[2:]
-    tot = sum(float(r[i] or 0) for r in data) or 1
-    print("hottest SASS (share of stall samples):")
-    for r in sorted(data, key=lambda r: -float(r[i] or 0))[:15]:
+    data = [r for r in sc["rows"][1:] if len(r) > i and r[i].replace(".", "").isdigit()]
+    tot = sum(float(r[i]) for r in data) or 1
+    print("hottest SASS (share of stall samples):", sc["name"][:60])
+    for r in sorted(data, key=lambda r: -float(r[i]))[:15]:
         print(f"  {float(r[i]) / tot * 100:5.1f}%  {r[1][:100]}")
+    break
