@@ -53,6 +53,8 @@ for st in settings:
     err = float(np.max(np.abs(yh - ref)) / max(1.0, float(np.max(np.abs(ref)))))
     print(f"{cfg} [{st}]: step {ms:.4f} ms {B / ms / 1e6:.0f} GB/s  phases main {ph[0]:.4f} finish {ph[1]:.4f} "
           f"rest {ph[2]:.4f} total {ph[3]:.4f}  diff-vs-first {err:.1e}", flush=True)
+    op.close()
     del op
+    getattr(s, "_device", {}).clear()  # (prepare caches the operator on the split)
     for k in kv:
         del os.environ[k]
