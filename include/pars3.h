@@ -304,6 +304,19 @@ int pars3_split_device(int64_t n, const int64_t *row_ptr, const int32_t *col_ind
 int pars3_bandwidth_device(int64_t n, const int64_t *row_ptr, const int32_t *col_ind,
                            int64_t *bandwidth, void *stream);
 
+/* classify_conflicts on the device (replaces split.py:303-361 /
+ * pars3_classify_conflicts when the split is device-resident, e.g. right after
+ * pars3_split_device).  Device arrays: mid_ptr [n+1], mid_col, row_owner [n],
+ * safe_start [n], conflict_idx / conflict_target / apply_order
+ * [conflict_count].  Host arrays: block_start [p+1], conflict_count,
+ * conflict_ptr [p+1], apply_ptr [p+1], halo_lo [p].  Call with conflict_idx ==
+ * NULL for the count.  Same arrays as the host function, bit for bit. */
+int pars3_classify_conflicts_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col, int64_t p,
+                                    const int64_t *block_start, int64_t *conflict_count,
+                                    int64_t *row_owner, int64_t *safe_start, int64_t *conflict_idx,
+                                    int64_t *conflict_ptr, int64_t *conflict_target, int64_t *apply_order,
+                                    int64_t *apply_ptr, int64_t *halo_lo, void *stream);
+
 /* Relabel an SSS matrix: replaces coo_to_sss(apply_permutation(coo, perm))
  * (reorder.py:289-297, formats.py:413-475) without the COO round trip.
  * Output arrays sized like the input. */

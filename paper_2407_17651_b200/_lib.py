@@ -102,6 +102,8 @@ _SIGS = {
     "pars3_split_device": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                           _vp, _vp, _vp]),
     "pars3_bandwidth_device": (ctypes.c_int, [_c_i64, _vp, _vp, ctypes.POINTER(_c_i64), _vp]),
+    "pars3_classify_conflicts_device": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, ctypes.POINTER(_c_i64)]
+                                        + [_vp] * 9),
     "pars3_permute_lower": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                            ctypes.c_int]),
     "pars3_split_count": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, ctypes.POINTER(_c_i64),

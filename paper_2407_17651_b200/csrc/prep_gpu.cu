@@ -9,6 +9,8 @@
 #include <cub/cub.cuh>
 
 #include <cstdint>
+#include <algorithm>
+#include <vector>
 
 #include "common.h"
 
@@ -231,5 +233,155 @@ extern "C" int pars3_bandwidth_device(int64_t n, const int64_t *row_ptr, const i
     RC(cudaMemcpyAsync(&h, d.p, sizeof(h), cudaMemcpyDeviceToHost, st));
     RC(cudaStreamSynchronize(st));
     *bandwidth = (int64_t)h;
+    return PARS3_OK;
+}
+
+// ---- classify_conflicts on the device (split.py:303-361) --------------------
+// A middle entry (i, c) is a conflict when its column belongs to an earlier
+// block than its row (c < block_start[owner(i)]): columns ascend within a
+// row, so a row's conflicts are a prefix of its middle entries.  Outputs as
+// the host version (prep.cpp, pars3_classify_conflicts), bit for bit:
+// conflict_idx ascending, apply_order the stable order by target block.
+namespace {
+
+__device__ __forceinline__ int owner_block(const int64_t *bs, int p, int64_t i) {
+    int lo = 0, hi = p;  // bs[lo] <= i < bs[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (bs[mid] <= i)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_cf_count(int64_t n, const int64_t *mp, const int32_t *mc, int p, const int64_t *bs,
+                           int64_t *ncf, int64_t *row_owner, int64_t *safe_start) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int w = owner_block(bs, p, i);
+        const int64_t lo = bs[w];
+        int64_t a = mp[i], b = mp[i + 1];  // first k in [a, b) with mc[k] >= lo
+        while (a < b) {
+            const int64_t mid = (a + b) >> 1;
+            if (mc[mid] < lo)
+                a = mid + 1;
+            else
+                b = mid;
+        }
+        ncf[i] = a - mp[i];
+        if (row_owner) {
+            row_owner[i] = w;
+            safe_start[i] = a;
+        }
+    }
+}
+
+__global__ void k_cf_fill(int64_t n, const int64_t *mp, const int32_t *mc, int p, const int64_t *bs,
+                          const int64_t *cfp, int64_t *conflict_idx, int64_t *conflict_target, int32_t *tkey,
+                          unsigned long long *incoming, unsigned long long *halo) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j0 = cfp[i], cnt = cfp[i + 1] - j0;
+        if (cnt == 0) continue;
+        const int w = owner_block(bs, p, i);
+        // the row's first conflict has its smallest column
+        atomicMin(&halo[w], (unsigned long long)mc[mp[i]]);
+        for (int64_t q = 0; q < cnt; q++) {
+            const int64_t k = mp[i] + q;
+            const int t = owner_block(bs, p, mc[k]);
+            conflict_idx[j0 + q] = k;
+            conflict_target[j0 + q] = t;
+            tkey[j0 + q] = t;
+            atomicAdd(&incoming[t], 1ull);
+        }
+    }
+}
+
+__global__ void k_iota64(int64_t m, int64_t *a) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) a[k] = k;
+}
+
+__global__ void k_gather64(int p1, const int64_t *src, const int64_t *idx, int64_t *dst) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w < p1) dst[w] = src[idx[w]];
+}
+
+}  // namespace
+
+// Device arrays: mid_ptr [n + 1], mid_col, and the outputs row_owner [n],
+// safe_start [n], conflict_idx / conflict_target / apply_order
+// [conflict_count].  Host arrays: block_start [p + 1], conflict_count,
+// conflict_ptr [p + 1], apply_ptr [p + 1], halo_lo [p].  Call with
+// conflict_idx == NULL for the count (row_owner / safe_start optional then).
+extern "C" int pars3_classify_conflicts_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
+                                               int64_t p, const int64_t *block_start, int64_t *conflict_count,
+                                               int64_t *row_owner, int64_t *safe_start, int64_t *conflict_idx,
+                                               int64_t *conflict_ptr, int64_t *conflict_target,
+                                               int64_t *apply_order, int64_t *apply_ptr, int64_t *halo_lo,
+                                               void *stream) {
+    if (p < 1 || p > (1 << 20) || !block_start || block_start[0] != 0 || block_start[p] != n || !conflict_count)
+        PARS3_FAIL(PARS3_ERR_STRUCT, "block_start must run from 0 to n over p blocks");
+    for (int64_t w = 0; w < p; w++)
+        if (block_start[w + 1] <= block_start[w]) PARS3_FAIL(PARS3_ERR_STRUCT, "every block must own at least one row");
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf<int64_t> bs, cfp;
+    RC(bs.alloc(p + 1));
+    RC(cfp.alloc(n + 1));
+    RC(cudaMemcpyAsync(bs.p, block_start, sizeof(int64_t) * (p + 1), cudaMemcpyHostToDevice, st));
+    RC(cudaMemsetAsync(cfp.p, 0, sizeof(int64_t), st));
+    const int G = blocks_for(n);
+    k_cf_count<<<G, kTB, 0, st>>>(n, mid_ptr, mid_col, (int)p, bs.p, cfp.p + 1, row_owner, safe_start);
+    RC(cudaGetLastError());
+    size_t tb = 0;
+    RC(cub::DeviceScan::InclusiveSum(nullptr, tb, cfp.p + 1, cfp.p + 1, n, st));
+    DevBuf<uint8_t> temp;
+    RC(temp.alloc(tb));
+    RC(cub::DeviceScan::InclusiveSum(temp.p, tb, cfp.p + 1, cfp.p + 1, n, st));
+    int64_t total = 0;
+    RC(cudaMemcpyAsync(&total, cfp.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    RC(cudaStreamSynchronize(st));
+    *conflict_count = total;
+    if (!conflict_idx) return PARS3_OK;
+    if (!row_owner || !safe_start || !conflict_ptr || !conflict_target || !apply_order || !apply_ptr || !halo_lo)
+        PARS3_FAIL(PARS3_ERR_ARG, "classify_conflicts_device: null output");
+    if (total >= INT32_MAX) PARS3_FAIL(PARS3_ERR_ARG, "classify_conflicts_device: too many conflicts");
+    // conflict_ptr[w] = conflicts of the rows below block w
+    DevBuf<int64_t> cpd;
+    RC(cpd.alloc(p + 1));
+    k_gather64<<<(int)((p + 1 + kTB - 1) / kTB), kTB, 0, st>>>((int)(p + 1), cfp.p, bs.p, cpd.p);
+    RC(cudaMemcpyAsync(conflict_ptr, cpd.p, sizeof(int64_t) * (p + 1), cudaMemcpyDeviceToHost, st));
+    DevBuf<unsigned long long> incoming, halo;
+    RC(incoming.alloc(p));
+    RC(halo.alloc(p));
+    RC(cudaMemsetAsync(incoming.p, 0, sizeof(unsigned long long) * p, st));
+    RC(cudaMemcpyAsync(halo.p, block_start, sizeof(int64_t) * p, cudaMemcpyHostToDevice, st));
+    std::vector<unsigned long long> hin(p), hhalo(p);
+    if (total > 0) {
+        DevBuf<int32_t> tkey, tkey2;
+        DevBuf<int64_t> iota;
+        RC(tkey.alloc(total));
+        RC(tkey2.alloc(total));
+        RC(iota.alloc(total));
+        k_cf_fill<<<G, kTB, 0, st>>>(n, mid_ptr, mid_col, (int)p, bs.p, cfp.p, conflict_idx, conflict_target,
+                                     tkey.p, incoming.p, halo.p);
+        k_iota64<<<blocks_for(total), kTB, 0, st>>>(total, iota.p);
+        RC(cudaGetLastError());
+        int bits = 1;
+        while ((1ll << bits) < p) bits++;
+        size_t ts = 0;
+        RC(cub::DeviceRadixSort::SortPairs(nullptr, ts, tkey.p, tkey2.p, iota.p, apply_order, (int)total, 0, bits, st));
+        DevBuf<uint8_t> temp2;
+        RC(temp2.alloc(ts));
+        RC(cub::DeviceRadixSort::SortPairs(temp2.p, ts, tkey.p, tkey2.p, iota.p, apply_order, (int)total, 0, bits, st));
+        RC(cudaStreamSynchronize(st));  // (the temporaries are freed on return)
+    }
+    RC(cudaMemcpyAsync(hin.data(), incoming.p, sizeof(unsigned long long) * p, cudaMemcpyDeviceToHost, st));
+    RC(cudaMemcpyAsync(hhalo.data(), halo.p, sizeof(unsigned long long) * p, cudaMemcpyDeviceToHost, st));
+    RC(cudaStreamSynchronize(st));
+    apply_ptr[0] = 0;
+    for (int64_t w = 0; w < p; w++) {
+        apply_ptr[w + 1] = apply_ptr[w] + (int64_t)hin[w];
+        halo_lo[w] = (int64_t)hhalo[w];
+    }
     return PARS3_OK;
 }

@@ -10,9 +10,10 @@
 with every stage on the device (csrc/rcm.cu, csrc/prep_gpu.cu): the
 skyline arrays are uploaded once, and only the results come back.  The
 returned objects are the host-chain's bit for bit (tests/test_gpu_rcm.py
-checks both chains, and the reference's SHA-256s for c2-c4).  The
-conflict plan (``classify_conflicts``) stays host-native: it is one pass
-over the middle band's row prefixes.
+checks both chains, and the reference's SHA-256s for c2-c5).
+``classify_conflicts_gpu`` / ``prepare_gpu(..., boundaries=...)`` run the
+conflict classification (split.py:303-361) on the device too, on the
+device-resident split.
 """
 
 from __future__ import annotations
@@ -26,7 +27,7 @@ from .formats import SssMatrix
 from .reorder import Permutation, _upload
 from .split import BandSplit, default_beta
 
-__all__ = ["prepare_gpu"]
+__all__ = ["prepare_gpu", "classify_conflicts_gpu"]
 
 _CHUNK = 64 << 20  # first-touch slice per thread task
 
@@ -70,8 +71,60 @@ def _download(tensors, torch):
     return outs
 
 
-def prepare_gpu(m0: SssMatrix, beta: int | None = None, device="cuda"):
-    """(perm, m, s, bandwidth) of the host chain, computed on the GPU."""
+def _classify_device(L, torch, dev, n, beta, mp, mc, boundaries, st):
+    """PartitionPlan of a device-resident split (mp, mc: device tensors)."""
+    from .split import PartitionPlan, StructuralError
+    bs = np.array(boundaries, dtype=np.int64).ravel()
+    p = bs.size - 1
+    if p < 1 or bs[0] != 0 or bs[-1] != n:
+        raise StructuralError("block_start must run from 0 to n over p blocks")
+    sizes = np.diff(bs)
+    if np.any(sizes < 1):
+        raise StructuralError("every block must own at least one row")
+    if sizes.max() - sizes.min() > 1:
+        raise StructuralError("block sizes must differ by at most one row")
+    k = _lib._c_i64()
+    ro = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    ss = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    head = (n, _lib.ptr(mp), _lib.ptr(mc), p, _lib.ptr(bs), ctypes.byref(k), _lib.ptr(ro), _lib.ptr(ss))
+    _lib.check(L.pars3_classify_conflicts_device(*head, None, None, None, None, None, None, st),
+               "classify_conflicts_gpu")
+    kk = int(k.value)
+    ci = torch.empty(max(kk, 1), dtype=torch.int64, device=dev)
+    ct = torch.empty(max(kk, 1), dtype=torch.int64, device=dev)
+    ao = torch.empty(max(kk, 1), dtype=torch.int64, device=dev)
+    cp = np.empty(p + 1, np.int64)
+    ap = np.empty(p + 1, np.int64)
+    hl = np.empty(p, np.int64)
+    _lib.check(L.pars3_classify_conflicts_device(*head, _lib.ptr(ci), _lib.ptr(cp), _lib.ptr(ct),
+                                                 _lib.ptr(ao), _lib.ptr(ap), _lib.ptr(hl), st),
+               "classify_conflicts_gpu")
+    h = _download((ro[:n], ss[:n], ci[:kk], ct[:kk], ao[:kk]), torch)
+    return PartitionPlan(n=n, p=p, beta=int(beta), block_start=bs, row_owner=h[0], safe_start=h[1],
+                         conflict_idx=h[2], conflict_ptr=cp, conflict_target=h[3], apply_order=h[4],
+                         apply_ptr=ap, halo_lo=hl)
+
+
+def classify_conflicts_gpu(s, boundaries, device="cuda"):
+    """``classify_conflicts`` (split.py:303-361) computed on the GPU: the same
+    PartitionPlan and ConflictReport as the host function, bit for bit."""
+    from .device import require_cuda
+    from .split import conflict_report
+    torch = require_cuda()
+    dev = torch.device(device)
+    L = _lib.load()
+    with torch.cuda.device(dev):
+        mp = _upload(s.mid_ptr, np.int64, dev)
+        mc = _upload(s.mid_col, np.int32, dev) if s.mid_col.size else torch.zeros(1, dtype=torch.int32, device=dev)
+        plan = _classify_device(L, torch, dev, s.n, s.beta, mp, mc, boundaries, _lib.stream_ptr())
+    return plan, conflict_report(s, plan)
+
+
+def prepare_gpu(m0: SssMatrix, beta: int | None = None, device="cuda", boundaries=None):
+    """(perm, m, s, bandwidth) of the host chain, computed on the GPU.  With
+    ``boundaries`` (a block partition, e.g. ``partition_rows(n, p)``) the
+    conflict classification runs on the device-resident split as well and
+    the result is (perm, m, s, bandwidth, plan)."""
     from .device import require_cuda
     torch = require_cuda()
     dev = torch.device(device)
@@ -119,8 +172,13 @@ def prepare_gpu(m0: SssMatrix, beta: int | None = None, device="cuda"):
         names, ts = zip(*(("fw", fw), ("rp", rp2), ("ci", ci2[:nnz]), ("od", od2[:nnz]),
                           ("dg", dg2[:n]), ("mp", mp), ("mc", mc[:nm]), ("mv", mv[:nm]),
                           ("orow", orow[:no]), ("ocol", ocol[:no]), ("oval", oval[:no])))
+        plan = None
+        if boundaries is not None:
+            plan = _classify_device(L, torch, dev, n, beta, mp, mc, boundaries, st)
         h = dict(zip(names, _download(ts, torch)))
     perm = Permutation(h["fw"])
     m = SssMatrix._trusted(n, h["rp"], h["ci"], h["od"], h["dg"])
     s = BandSplit(n, int(beta), h["dg"], h["mp"], h["mc"], h["mv"], h["orow"], h["ocol"], h["oval"])
+    if boundaries is not None:
+        return perm, m, s, bw, plan
     return perm, m, s, bw

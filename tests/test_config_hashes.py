@@ -128,6 +128,9 @@ def test_gpu_chain_hashes_c5(lib_built, golden_hashes):
     g = G.make_config("c5")
     m0 = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
     del g
-    perm, m, s, bw = prepare_gpu(m0)
+    perm, m, s, bw, plan8 = prepare_gpu(m0, boundaries=P.partition_rows(m0.n, 8))
     assert bw == h["bandwidth"]
+    # classify_conflicts on the device-resident split (p = 8), then the host function (every p)
+    for f in PLAN_FIELDS:
+        assert sha(getattr(plan8, f)) == h[f"b{s.beta}/p8/{f}"], ("gpu classify", f)
     _check_chain_c5(h, perm, m, s, s.beta)

@@ -127,3 +127,41 @@ def test_page_locked_download(lib_built):
         assert o.dtype == h.dtype and o.shape == h.shape
         assert np.array_equal(o, h)
         assert o.flags.writeable and o.flags.c_contiguous
+
+
+@pytest.mark.parametrize("name,m", [(n, m) for n, m in _graphs()
+                                    if n in ("rmat12", "band", "stencil27", "grid5", "small_components",
+                                             "single")],
+                         ids=lambda v: v if isinstance(v, str) else "")
+@pytest.mark.parametrize("p", [1, 2, 3, 8])
+def test_gpu_classify_equals_host(name, m, p, lib_built):
+    """classify_conflicts on the device (split.py:303-361): every PartitionPlan
+    array and the ConflictReport equal to the host-native function's, both
+    standalone and inside prepare_gpu (device-resident split)."""
+    from conftest import PLAN_FIELDS
+    from paper_2407_17651_b200.pipeline import classify_conflicts_gpu, prepare_gpu
+    perm = P.rcm_order(P.pattern_from_sss(m))
+    mh = P.permute_sss(m, perm)
+    if p > mh.n:
+        pytest.skip("more workers than rows")
+    for beta in (None, 3):
+        b = P.default_beta(mh.n, P.compute_bandwidth(mh)) if beta is None else beta
+        sh = P.split_bands(mh, b)
+        bounds = P.partition_rows(mh.n, p)
+        want, wrep = P.classify_conflicts(sh, bounds)
+        got, grep = classify_conflicts_gpu(sh, bounds)
+        chain = prepare_gpu(m, beta, boundaries=bounds)[4]
+        for f in PLAN_FIELDS:
+            assert np.array_equal(getattr(got, f), getattr(want, f)), (name, p, f)
+            assert np.array_equal(getattr(chain, f), getattr(want, f)), (name, p, f, "chain")
+        assert grep == wrep
+
+
+def test_gpu_classify_errors(lib_built):
+    from paper_2407_17651_b200.pipeline import classify_conflicts_gpu
+    from paper_2407_17651_b200 import generators as G
+    m = _sss(G.grid5(12, seed_perm=1, seed_val=2))
+    s = P.split_bands(m, 5)
+    for bad in ([0, 10], [1, m.n], [0, 5, 5, m.n], [0, 1, m.n]):
+        with pytest.raises(P.StructuralError):
+            classify_conflicts_gpu(s, bad)
