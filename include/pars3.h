@@ -103,6 +103,10 @@ typedef struct pars3_plan_options {
  * NO_DIRECT forbids it (peer mode and SKIP_EMPTY plans never use it). */
 #define PARS3_PLAN_DIRECT 32
 #define PARS3_PLAN_NO_DIRECT 64
+/* The tile plan is built on the device when it can be (window-mode plans:
+ * csrc/tileplan_gpu.cu, the host builder's arrays byte for byte); HOST_BUILD
+ * forces the host builder (csrc/tileplan.cpp). */
+#define PARS3_PLAN_HOST_BUILD 128
 
 /* The internal locality order a plan may use (host only; for inspection and
  * tests): forward[split label] = internal label; *dropped = directed edges
@@ -216,11 +220,26 @@ int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *c
 /* Device bytes held by the plan. */
 int pars3_plan_bytes(const pars3_plan *plan, int64_t *bytes);
 
-/* stats[14] = {tiles, slices, padded slots, stored entries, windows,
+/* stats[19] = {tiles, slices, padded slots, stored entries, windows,
  * max local slots, grid CTAs, device bytes, list-mode tiles, accumulator
  * words (0 = fp64, 2 or 3 = fixed point), locality order (0/1), shared-memory
- * slots over all tiles, edges the locality filter dropped, direct mode (0/1)}. */
+ * slots over all tiles, edges the locality filter dropped, direct mode (0/1),
+ * grid form (0/1), grid headroom bits, grid deliveries per row block, grid
+ * value exponent, tile plan built on the device (0/1)}. */
 int pars3_plan_stats(const pars3_plan *plan, int64_t *stats);
+
+/* Inspection / tests: the tile plan of a split as host arrays,
+ * from the host builder (use_device = 0, csrc/tileplan.cpp) or the device
+ * builder (1, csrc/tileplan_gpu.cu; PARS3_ERR_ARG when it does not support
+ * the plan), with the option set pars3_plan_create derives for `words`
+ * accumulator words (2, 3, or 0 = fp64).  sizes[9] = {tiles, windows, slices,
+ * record bytes, stored entries, padded slots, max terms per slot, list-mode
+ * tiles, list columns}.  Call with tiles == NULL for the sizes, then with
+ * arrays: tiles (48 B each), wins (16 B each), slice_off (slices + 1), rec
+ * (record bytes), ucol (list columns). */
+int pars3_tile_plan_arrays(const pars3_split_view *split, const pars3_plan_options *opt, int32_t words,
+                           int32_t use_device, int64_t *sizes, void *tiles, void *wins,
+                           int64_t *slice_off, uint8_t *rec, int32_t *ucol);
 int pars3_plan_destroy(pars3_plan *plan);
 
 /* Debug: per-phase SM-cycle totals of the tile kernel's thread 0 (plan

@@ -52,6 +52,7 @@ PLAN_LOCALITY = 8      # try the internal locality order on every plan (pars3.h)
 PLAN_NO_LOCALITY = 16  # never use it
 PLAN_DIRECT = 32       # direct mode (no shared staging) forced (pars3.h)
 PLAN_NO_DIRECT = 64    # never direct mode
+PLAN_HOST_BUILD = 128  # tile plan by the host builder (never csrc/tileplan_gpu.cu)
 PRODUCT_ACC = 1        # pars3_plan_product: y += A x
 PRODUCT_STRICT = 2     # the grid scale from this x (a pure function of x)
 
@@ -76,6 +77,7 @@ _SIGS = {
     "pars3_plan_bytes": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i64)]),
     "pars3_dot": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
     "pars3_plan_stats": (ctypes.c_int, [_vp, _vp]),
+    "pars3_tile_plan_arrays": (ctypes.c_int, [_vp, _vp, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_locality_order": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, ctypes.POINTER(_c_i64)]),
     "pars3_full_csr_host": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_plan_profile": (ctypes.c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _vp, _vp]),

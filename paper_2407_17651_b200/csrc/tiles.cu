@@ -36,6 +36,7 @@
 //      NVLink.  Exact (the same per-tile guard), not bitwise repeatable.
 
 #include <cuda_runtime.h>
+#include <omp.h>
 
 #include <cmath>
 #include <cstdint>
@@ -67,6 +68,7 @@
 #endif
 #include "locality.h"
 #include "tileplan.h"
+#include "tileplan_gpu.h"
 
 using pars3::LocalityOrder;
 using pars3::HostPlan;
@@ -1296,6 +1298,7 @@ struct pars3_plan {
     double *xs = nullptr, *ys = nullptr;
     int64_t local_slots = 0, dropped = 0;
     // row-major form (k_csr): the full CSR of A in lanes of 16 entries, no tiles
+    int32_t built_on_device = 0;  // the tile plan came from tileplan_gpu.cu
     int32_t direct = 0, nspan = 0;
     int64_t ne = 0, nwarps = 0;
     int32_t *ccol = nullptr, *clrow = nullptr, *span_row = nullptr, *span_w0 = nullptr, *span_w1 = nullptr;
@@ -1431,22 +1434,51 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     // when the plan allows, else three words (<= 4096 terms; exact integer
     // sums keep the product bitwise repeatable), else fp64
     const int req_mode = opt ? opt->mode : 0;
+    // PARS3_VERBOSE=1: wall-clock of the plan's phases on stderr
+    const bool verbose = getenv("PARS3_VERBOSE") != nullptr;
+    double t_prev = omp_get_wtime();
+    auto lap = [&](const char *what) {
+        const double now = omp_get_wtime();
+        if (verbose) fprintf(stderr, "pars3 plan: %-28s %.3f s\n", what, now - t_prev);
+        t_prev = now;
+    };
     const bool safe_values = values_fixed_point_safe(s);
+    lap("value range check");
     int words0 = req_mode == 1 ? 3 : req_mode == 2 ? 0 : 2;
     if (words0 && !safe_values) words0 = 0;  // fp64 accumulators keep IEEE semantics
     // the shared-memory budget (x + accumulators per slot, 4 CTAs / SM) caps both
     if (o0.seg_max > 8) o0.seg_max = 8;
     const int32_t want_local = o0.local_slots;
     o0.max_segments = std::min(o0.max_segments, 32 * kMaxTileSlices);
-    auto build = [&](const pars3_split_view *v, PlanOptions &o, int &words, HostPlan &hp) -> int {
+    // The tile plan is built on the device when it can be (window-mode
+    // plans: tileplan_gpu.cu, the same arrays byte for byte, left on the
+    // device in `dp`), else by the host builder.  PARS3_PLAN_HOST=1 /
+    // PARS3_PLAN_HOST_BUILD: always the host builder.
+    const char *ph_env = getenv("PARS3_PLAN_HOST");
+    const bool may_device = !(ph_env && ph_env[0] == '1') && !(flags & PARS3_PLAN_HOST_BUILD);
+    auto tile_plan = [&](const pars3_split_view *v, const PlanOptions &o, HostPlan &hp, pars3::DevicePlan *dp) -> int {
+        if (dp) {
+            dp->release();
+            bool ok = false;
+            if (may_device) {
+                const int rc = pars3::build_tile_plan_device(v->n, v->mid_ptr, v->mid_col, v->mid_val, v->outer_count,
+                                                             v->outer_row, v->outer_col, v->outer_val, o, hp, *dp, ok);
+                if (rc) return rc;
+            }
+            if (ok) return PARS3_OK;
+        }
+        return pars3::build_tile_plan(v->n, v->mid_ptr, v->mid_col, v->mid_val, v->outer_count, v->outer_row,
+                                      v->outer_col, v->outer_val, o, hp);
+    };
+    auto build = [&](const pars3_split_view *v, PlanOptions &o, int &words, HostPlan &hp,
+                     pars3::DevicePlan *dp) -> int {
         o = o0;
         words = words0;
         o.terms_cap = words == 2 ? kTerms2 : 0;
         if (const char *ts = getenv("PARS3_TERMS_MIN_ROWS")) o.terms_min_rows = atoi(ts);  // tuning knob
         o.local_slots = std::min(want_local, words == 3 ? kLocalFixed : kLocalExact);
         o.sink = (uint16_t)(words == 3 ? Layout<3>::kSink : Layout<0>::kSink);
-        int rc = pars3::build_tile_plan(v->n, v->mid_ptr, v->mid_col, v->mid_val, v->outer_count,
-                                        v->outer_row, v->outer_col, v->outer_val, o, hp);
+        int rc = tile_plan(v, o, hp, dp);
         if (rc) return rc;
         if (words == 2 && hp.max_terms > kTerms2) {
             if (req_mode == 3)
@@ -1457,8 +1489,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
             o.local_slots = std::min(want_local, kLocalFixed);
             o.sink = (uint16_t)Layout<3>::kSink;
             hp = HostPlan();
-            rc = pars3::build_tile_plan(v->n, v->mid_ptr, v->mid_col, v->mid_val, v->outer_count,
-                                        v->outer_row, v->outer_col, v->outer_val, o, hp);
+            rc = tile_plan(v, o, hp, dp);
             if (rc) return rc;
         }
         // the three 20-bit limbs carry <= 4096 terms per slot and tile
@@ -1478,8 +1509,14 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     PlanOptions o;
     int words = 0;
     HostPlan hp;
-    int rc = build(s, o, words, hp);
+    struct DpGuard {  // (frees the device-built arrays unless the plan takes them)
+        pars3::DevicePlan d;
+        ~DpGuard() { d.release(); }
+    } dpg;
+    pars3::DevicePlan &dp = dpg.d;
+    int rc = build(s, o, words, hp, &dp);
     if (rc) return rc;
+    lap(dp.rec ? "tile plan (device)" : "tile plan (host)");
     int64_t local = local_of(hp);
     // internal locality order (locality.cpp): tried when most tiles are
     // unstructured list tiles whose slots hold few entries each, kept when
@@ -1496,10 +1533,11 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         PlanOptions o2;
         int words2 = 0;
         HostPlan hp2;
-        rc = build(&v, o2, words2, hp2);
+        rc = build(&v, o2, words2, hp2, nullptr);
         if (rc) return rc;
         const int64_t local2 = local_of(hp2);
         if (10 * local2 < 7 * local) {
+            dp.release();
             o = o2;
             words = words2;
             hp = std::move(hp2);
@@ -1536,6 +1574,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         const int64_t m_entries = hp.nnz;
         hp = HostPlan();  // no tiles are uploaded
         hp.nnz = m_entries;
+        dp.release();
     }
     // grid form: single-GPU tile plans over finite, fixed-point-safe values
     // where every row belongs to a tile
@@ -1548,6 +1587,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
             PARS3_FAIL(PARS3_ERR_NOMEM, "out of host memory");
         }
         if (rc) return rc;
+        lap("grid bounds");
     }
     pars3_plan *pl = new (std::nothrow) pars3_plan;
     if (!pl) PARS3_FAIL(PARS3_ERR_NOMEM, "out of host memory");
@@ -1555,7 +1595,8 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     pl->beta = s->beta;
     pl->p = p;
     pl->ntiles = (int32_t)hp.tiles.size();
-    pl->nslices = std::max<int32_t>(0, (int32_t)hp.slice_off.size() - 1);
+    pl->nslices = dp.rec ? (int32_t)dp.nslices : std::max<int32_t>(0, (int32_t)hp.slice_off.size() - 1);
+    pl->built_on_device = dp.rec ? 1 : 0;
     pl->lmax = hp.max_local;
     pl->nnz = hp.nnz;
     pl->slots = hp.slots;
@@ -1618,10 +1659,20 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
         ZALLOC(whead, std::max<int64_t>(1, pl->nwarps));
         ZALLOC(wtail, std::max<int64_t>(1, pl->nwarps));
     }
-    UP(tiles, hp.tiles);
-    UP(wins, hp.wins);
-    UP(slice_off, hp.slice_off);
-    UP(rec, hp.rec);
+    if (dp.rec) {  // built on the device: the plan takes the arrays
+        pl->tiles = dp.tiles;
+        pl->wins = dp.wins;
+        pl->slice_off = dp.slice_off;
+        pl->rec = dp.rec;
+        pl->bytes += (int64_t)(sizeof(TileMeta) * dp.ntiles + sizeof(Window) * dp.nwins +
+                               sizeof(int64_t) * (dp.nslices + 1) + dp.rec_bytes);
+        dp = pars3::DevicePlan();
+    } else {
+        UP(tiles, hp.tiles);
+        UP(wins, hp.wins);
+        UP(slice_off, hp.slice_off);
+        UP(rec, hp.rec);
+    }
     UP(ucol, hp.ucol);
     if (!pl->diag_const) UP(diag, diag);
     if (!lo.forward.empty()) {
@@ -1689,6 +1740,7 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
     if (max_ctas > 0 && pl->grid > max_ctas) pl->grid = max_ctas;
     if (pl->grid > pl->ntiles) pl->grid = pl->ntiles > 0 ? pl->ntiles : 1;
     pl->grid_redo = std::min(pl->grid, per_sm_redo * sms);
+    lap("upload");
     *out = pl;
     return PARS3_OK;
 }
@@ -2039,6 +2091,73 @@ extern "C" int pars3_plan_stats(const pars3_plan *pl, int64_t *stats) {
     stats[15] = pl->hgrid;
     stats[16] = pl->cmax;
     stats[17] = pl->ev_g;
+    stats[18] = pl->built_on_device;
+    return PARS3_OK;
+}
+
+// Inspection / tests: the tile plan of a split as host arrays, built by the
+// host builder (use_device = 0) or by the device builder (1: PARS3_ERR_ARG
+// when it does not support the plan), with the option set pars3_plan_create
+// derives for `words` accumulator words (2, 3 or 0 = fp64).  sizes[9] =
+// {tiles, windows, slices, record bytes, stored entries, padded slots, max
+// terms, list tiles, list columns}; call with tiles == NULL for the sizes,
+// then with arrays (tiles: 48 B each, wins: 16 B each, slice_off: slices + 1).
+extern "C" int pars3_tile_plan_arrays(const pars3_split_view *s, const pars3_plan_options *opt, int32_t words,
+                                      int32_t use_device, int64_t *sizes, void *tiles, void *wins,
+                                      int64_t *slice_off, uint8_t *rec, int32_t *ucol) {
+    if (!s || !sizes || (words != 0 && words != 2 && words != 3)) PARS3_FAIL(PARS3_ERR_ARG, "bad argument");
+    PlanOptions o;
+    if (opt) {
+        if (opt->tile_rows > 0) o.tile_rows = opt->tile_rows;
+        if (opt->local_slots > 0) o.local_slots = opt->local_slots;
+        if (opt->seg_max > 0) o.seg_max = opt->seg_max;
+        if (opt->gap >= 0) o.gap = opt->gap;
+    }
+    if (o.seg_max > 8) o.seg_max = 8;
+    o.max_segments = std::min(o.max_segments, 32 * kMaxTileSlices);
+    o.terms_cap = words == 2 ? kTerms2 : 0;
+    o.local_slots = std::min(o.local_slots, words == 3 ? kLocalFixed : kLocalExact);
+    o.sink = (uint16_t)(words == 3 ? Layout<3>::kSink : Layout<0>::kSink);
+    HostPlan hp;
+    pars3::DevicePlan dp;
+    if (use_device) {
+        bool ok = false;
+        const int rc = pars3::build_tile_plan_device(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
+                                                     s->outer_row, s->outer_col, s->outer_val, o, hp, dp, ok);
+        if (rc) return rc;
+        if (!ok) PARS3_FAIL(PARS3_ERR_ARG, "the device builder does not support this plan");
+    } else {
+        const int rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count,
+                                              s->outer_row, s->outer_col, s->outer_val, o, hp);
+        if (rc) return rc;
+    }
+    const int64_t ns = use_device ? dp.nslices : (int64_t)hp.slice_off.size() - 1;
+    const int64_t nv = use_device ? dp.rec_bytes : (int64_t)hp.rec.size();
+    sizes[0] = (int64_t)hp.tiles.size();
+    sizes[1] = (int64_t)hp.wins.size();
+    sizes[2] = ns;
+    sizes[3] = nv;
+    sizes[4] = hp.nnz;
+    sizes[5] = hp.slots;
+    sizes[6] = hp.max_terms;
+    sizes[7] = hp.list_tiles;
+    sizes[8] = (int64_t)hp.ucol.size();
+    int rc = PARS3_OK;
+    if (tiles) {
+        std::memcpy(tiles, hp.tiles.data(), sizeof(TileMeta) * hp.tiles.size());
+        std::memcpy(wins, hp.wins.data(), sizeof(Window) * hp.wins.size());
+        if (ucol) std::memcpy(ucol, hp.ucol.data(), sizeof(int32_t) * hp.ucol.size());
+        if (use_device) {
+            if (cudaMemcpy(slice_off, dp.slice_off, sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToHost) != cudaSuccess ||
+                cudaMemcpy(rec, dp.rec, (size_t)nv, cudaMemcpyDeviceToHost) != cudaSuccess)
+                rc = PARS3_ERR_CUDA;
+        } else {
+            std::memcpy(slice_off, hp.slice_off.data(), sizeof(int64_t) * (ns + 1));
+            std::memcpy(rec, hp.rec.data(), (size_t)nv);
+        }
+    }
+    dp.release();
+    if (rc) PARS3_FAIL(rc, "pars3_tile_plan_arrays: download failed");
     return PARS3_OK;
 }
 
