@@ -137,7 +137,8 @@ def build_problem(cfg: str, beta=None, use_gpu=True):
         # the whole chain on the device (same arrays as the host chain:
         # tests/test_gpu_rcm.py), only the results come back
         from paper_2407_17651_b200.pipeline import prepare_gpu
-        perm, m, s, bw = prepare_gpu(m0, beta)
+        # (the split stays on the device for the plan build: no second upload)
+        perm, m, s, bw = prepare_gpu(m0, beta, keep_device=True)
         beta = s.beta
         t2 = t3 = time.time()
     else:

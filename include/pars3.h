@@ -123,6 +123,16 @@ int pars3_locality_order(const pars3_split_view *split, int64_t *forward, int64_
 int pars3_plan_create(const pars3_split_view *split, const pars3_plan_options *options,
                       int32_t p, const int64_t *block_start, pars3_plan **out, void *stream);
 
+/* The same with the split also resident on the current device (`resident`:
+ * a pars3_split_view of DEVICE pointers to the same arrays, e.g. the outputs
+ * of pars3_split_device; diag unused; NULL = pars3_plan_create): the tile
+ * plan is then built from the device copies without uploading the host
+ * arrays again (csrc/tileplan_gpu.cu).  The host view is still required (the
+ * plan's bounds and the fallback builders read it). */
+int pars3_plan_create_resident(const pars3_split_view *split, const pars3_split_view *resident,
+                               const pars3_plan_options *options, int32_t p, const int64_t *block_start,
+                               pars3_plan **plan, void *stream);
+
 /* Peer mode (multi-GPU, one process per GPU): the plan covers rank `me`'s
  * extended range [col_base, col_base + n) of global columns (built with
  * PARS3_PLAN_CUT_BLOCKS and the same block_start).  x_ptrs[r] is rank r's x

@@ -64,6 +64,9 @@ _SIGS = {
     "pars3_sss_spmv_atomic": (ctypes.c_int, [_c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_plan_create": (ctypes.c_int, [ctypes.POINTER(SplitView), ctypes.POINTER(PlanOptions),
                                          _c_i32, _vp, ctypes.POINTER(_vp), _vp]),
+    "pars3_plan_create_resident": (ctypes.c_int, [ctypes.POINTER(SplitView), ctypes.POINTER(SplitView),
+                                                  ctypes.POINTER(PlanOptions), _c_i32, _vp,
+                                                  ctypes.POINTER(_vp), _vp]),
     "pars3_plan_spmv": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "pars3_plan_spmv_acc": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "pars3_plan_set_peers": (ctypes.c_int, [_vp, _c_i32, _c_i32, _c_i64, _vp, _vp, _vp]),

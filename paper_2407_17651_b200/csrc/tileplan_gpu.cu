@@ -19,11 +19,14 @@
 //                  terms per slot, the value bound, the bank-spread slot
 //                  order of each slice (spread_banks, one thread per slice)
 #include <cuda_runtime.h>
+#include <omp.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.h"
@@ -782,7 +785,7 @@ void DevicePlan::release() {
 int build_tile_plan_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col, const double *mid_val,
                            int64_t outer_count, const int32_t *outer_row, const int32_t *outer_col,
                            const double *outer_val, const PlanOptions &o, HostPlan &P, DevicePlan &D,
-                           bool &supported) {
+                           bool &supported, const DeviceSplit *resident) {
     supported = false;
     D = DevicePlan();
     if (n < 1 || n >= INT32_MAX) return PARS3_OK;
@@ -790,19 +793,47 @@ int build_tile_plan_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid
         o.seg_max > 8 || o.gap < 2 /* (smaller gaps: alignment can merge runs) */ || o.gap > 20 || o.local_slots > 4094 || o.local_slots < 64 ||
         o.max_segments > 32 * PARS3_GPU_MAX_SLICES || o.sink == kNoSlot || o.sink < o.local_slots)
         return PARS3_OK;
+    const bool verbose = getenv("PARS3_VERBOSE") != nullptr;
+    double t_prev = omp_get_wtime();
+    auto lap = [&](const char *what) {
+        if (!verbose) return;
+        cudaDeviceSynchronize();
+        const double now = omp_get_wtime();
+        fprintf(stderr, "pars3 plan:   device builder: %-14s %.3f s\n", what, now - t_prev);
+        t_prev = now;
+    };
     const int64_t nm = mid_ptr[n];
     Buf<int64_t> mptr, optr;
     Buf<int32_t> mcol, ocol, orow;
     Buf<double> mval, oval;
     int rc;
-    if ((rc = to_device(mptr, mid_ptr, n + 1)) || (rc = to_device(mcol, mid_col, nm)) ||
-        (rc = to_device(mval, mid_val, nm)) || (rc = to_device(orow, outer_row, outer_count)) ||
-        (rc = to_device(ocol, outer_col, outer_count)) || (rc = to_device(oval, outer_val, outer_count)))
-        return rc;
+    Split S{};
+    S.n = n;
+    const int32_t *d_orow = nullptr;
+    if (resident) {  // the split is already on this device (prepare_gpu)
+        S.mptr = resident->mid_ptr;
+        S.mcol = resident->mid_col;
+        S.mval = resident->mid_val;
+        S.ocol = resident->outer_col;
+        S.oval = resident->outer_val;
+        d_orow = resident->outer_row;
+    } else {
+        if ((rc = to_device(mptr, mid_ptr, n + 1)) || (rc = to_device(mcol, mid_col, nm)) ||
+            (rc = to_device(mval, mid_val, nm)) || (rc = to_device(orow, outer_row, outer_count)) ||
+            (rc = to_device(ocol, outer_col, outer_count)) || (rc = to_device(oval, outer_val, outer_count)))
+            return rc;
+        S.mptr = mptr.p;
+        S.mcol = mcol.p;
+        S.mval = mval.p;
+        S.ocol = ocol.p;
+        S.oval = oval.p;
+        d_orow = orow.p;
+        lap("upload split");
+    }
     RC(optr.alloc(n + 1));
-    k_optr<<<(int)std::min<int64_t>((n + kT) / kT, 148 * 32), kT>>>(n, outer_count, orow.p, optr.p);
+    k_optr<<<(int)std::min<int64_t>((n + kT) / kT, 148 * 32), kT>>>(n, outer_count, d_orow, optr.p);
     RC(cudaGetLastError());
-    Split S{n, mptr.p, mcol.p, mval.p, optr.p, ocol.p, oval.p};
+    S.optr = optr.p;
     Opts oo{o.tile_rows, o.local_slots, o.seg_max, o.gap, o.max_segments, o.terms_cap, o.terms_min_rows, o.sink};
     const int64_t nranges = (n + o.tile_rows - 1) / o.tile_rows;
     Buf<DraftTile> draft;
@@ -817,6 +848,7 @@ int build_tile_plan_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid
     RC(cudaGetLastError());
     int32_t hf[8] = {0};
     RC(cudaMemcpy(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost));
+    lap("draft");
     const int32_t hflags = hf[0];
     if (hflags) {  // the host builder takes this plan
         if (getenv("PARS3_VERBOSE"))
@@ -881,6 +913,7 @@ int build_tile_plan_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid
                                                           wins.p, slice_off.p, rec.p, ucol.p, tot.p);
         RC(cudaGetLastError());
     }
+    lap("materialise");
     const int64_t end16 = nv / 16;
     RC(cudaMemcpy(slice_off.p + ns, &end16, sizeof(int64_t), cudaMemcpyHostToDevice));
     Totals ht{};
@@ -902,6 +935,7 @@ int build_tile_plan_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid
         P.max_local = std::max(P.max_local, m.local);
         P.list_tiles += m.u0 >= 0 ? 1 : 0;
     }
+    lap("download");
     D.ntiles = nt;
     D.nwins = nw;
     D.nslices = ns;

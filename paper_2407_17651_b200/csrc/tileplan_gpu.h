@@ -18,13 +18,21 @@ struct DevicePlan {  // device arrays of a plan built on the device (owned until
     void release();
 };
 
-// Host split arrays in (uploaded once), device plan out.  `supported` false:
+struct DeviceSplit {  // the split's arrays on the current device (optional: saves the upload)
+    const int64_t *mid_ptr;
+    const int32_t *mid_col;
+    const double *mid_val;
+    const int32_t *outer_row, *outer_col;
+    const double *outer_val;
+};
+
+// Host split arrays in (uploaded once unless `resident` holds them), device plan out.  `supported` false:
 // this plan needs the host builder (build_tile_plan); nothing is returned
 // then.  On success P holds the small host-side parts (tiles, windows,
 // totals; no records) and D the device arrays.
 int build_tile_plan_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col, const double *mid_val,
                            int64_t outer_count, const int32_t *outer_row, const int32_t *outer_col,
                            const double *outer_val, const PlanOptions &opt, HostPlan &P, DevicePlan &D,
-                           bool &supported);
+                           bool &supported, const DeviceSplit *resident = nullptr);
 
 }  // namespace pars3

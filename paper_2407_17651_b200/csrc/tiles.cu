@@ -1344,10 +1344,14 @@ static int grid_data(const pars3_split_view *v, const HostPlan &hp, GridData &G)
     const int64_t n = v->n;
     const int64_t nt = (int64_t)hp.tiles.size();
     std::vector<int32_t> blk(n, -1);
+#pragma omp parallel for schedule(dynamic, 256)
     for (int64_t t = 0; t < nt; t++)
         for (int32_t r = hp.tiles[t].r0; r < hp.tiles[t].r1; r++) blk[r] = (int32_t)t;
+    int64_t orphan = -1;
+#pragma omp parallel for schedule(static) reduction(max : orphan)
     for (int64_t r = 0; r < n; r++)
-        if (blk[r] < 0) PARS3_FAIL(PARS3_ERR_STRUCT, "grid form: row %lld belongs to no tile", (long long)r);
+        if (blk[r] < 0) orphan = std::max(orphan, r);
+    if (orphan >= 0) PARS3_FAIL(PARS3_ERR_STRUCT, "grid form: row %lld belongs to no tile", (long long)orphan);
     std::vector<std::vector<int32_t>> lists(nt);
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t t = 0; t < nt; t++) {
@@ -1383,14 +1387,23 @@ static int grid_data(const pars3_split_view *v, const HostPlan &hp, GridData &G)
     // terms per y element: row entries + column mirrors + the diagonal
     std::vector<int32_t> terms(n, 1);
     const int64_t nm = v->mid_ptr ? v->mid_ptr[n] : 0;
+#pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < n; r++) terms[r] += (int32_t)(v->mid_ptr[r + 1] - v->mid_ptr[r]);
-    for (int64_t k = 0; k < nm; k++) terms[v->mid_col[k]]++;
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < nm; k++) {
+#pragma omp atomic
+        terms[v->mid_col[k]]++;
+    }
+#pragma omp parallel for schedule(static)
     for (int64_t k = 0; k < v->outer_count; k++) {
+#pragma omp atomic
         terms[v->outer_row[k]]++;
+#pragma omp atomic
         terms[v->outer_col[k]]++;
     }
     int64_t dmax = 1;
     double dg = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : dmax, dg)
     for (int64_t r = 0; r < n; r++) {
         dmax = std::max<int64_t>(dmax, terms[r]);
         dg = std::max(dg, std::fabs(v->diag[r]));
@@ -1407,7 +1420,15 @@ static int grid_data(const pars3_split_view *v, const HostPlan &hp, GridData &G)
 extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_options *opt,
                                  int32_t p, const int64_t *block_start, pars3_plan **out,
                                  void *stream) {
+    return pars3_plan_create_resident(s, nullptr, opt, p, block_start, out, stream);
+}
+
+extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3_split_view *resident,
+                                          const pars3_plan_options *opt, int32_t p,
+                                          const int64_t *block_start, pars3_plan **out, void *stream) {
     (void)stream;
+    if (resident && s && (resident->n != s->n || resident->outer_count != s->outer_count || !resident->mid_ptr))
+        PARS3_FAIL(PARS3_ERR_ARG, "the device-resident split does not match the host split");
     if (!s || !out) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
     *out = nullptr;
     if (s->n < 0 || s->n >= INT32_MAX || s->beta < 1) PARS3_FAIL(PARS3_ERR_ARG, "bad split header");
@@ -1461,8 +1482,13 @@ extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_opt
             dp->release();
             bool ok = false;
             if (may_device) {
+                pars3::DeviceSplit ds{};
+                if (resident && v == s)
+                    ds = pars3::DeviceSplit{resident->mid_ptr, resident->mid_col, resident->mid_val,
+                                            resident->outer_row, resident->outer_col, resident->outer_val};
                 const int rc = pars3::build_tile_plan_device(v->n, v->mid_ptr, v->mid_col, v->mid_val, v->outer_count,
-                                                             v->outer_row, v->outer_col, v->outer_val, o, hp, *dp, ok);
+                                                             v->outer_row, v->outer_col, v->outer_val, o, hp, *dp, ok,
+                                                             resident && v == s ? &ds : nullptr);
                 if (rc) return rc;
             }
             if (ok) return PARS3_OK;

@@ -38,7 +38,11 @@ class Pars3Operator:
     """y = A x on one GPU for a (diag, middle, outer) decomposition of A."""
 
     def __init__(self, n, beta, diag, mid_ptr, mid_col, mid_val, outer_row, outer_col, outer_val,
-                 p=1, block_start=None, device=None, options=None):
+                 p=1, block_start=None, device=None, options=None, resident=None):
+        """``resident``: optional dict of CUDA tensors holding the same split on
+        this device (mid_ptr int64, mid_col int32, mid_val float64, outer_row /
+        outer_col int32, outer_val float64; ``prepare_gpu(..., keep_device=True)``):
+        the tile plan is then built from them without another upload."""
         torch = require_cuda()
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
@@ -61,9 +65,20 @@ class Pars3Operator:
         bs = _c(block_start if block_start is not None else [0, self.n], np.int64)
         handle = ctypes.c_void_p()
         L = _lib.load()
+        rview = None
+        if resident is not None and all(resident[k].device == self.device for k in resident):
+            r = resident
+            if (r["mid_ptr"].numel() == self.n + 1 and r["mid_col"].numel() >= host["mid_col"].size
+                    and r["outer_col"].numel() >= host["outer_col"].size):
+                rview = _lib.SplitView(self.n, self.beta, None, _lib.ptr(r["mid_ptr"]), _lib.ptr(r["mid_col"]),
+                                       _lib.ptr(r["mid_val"]), int(host["outer_col"].size),
+                                       _lib.ptr(r["outer_row"]), _lib.ptr(r["outer_col"]),
+                                       _lib.ptr(r["outer_val"]))
         with torch.cuda.device(self.device):
-            _lib.check(L.pars3_plan_create(ctypes.byref(view), ctypes.byref(opts), self.p,
-                                           _lib.ptr(bs), ctypes.byref(handle), None),
+            _lib.check(L.pars3_plan_create_resident(ctypes.byref(view),
+                                                    ctypes.byref(rview) if rview is not None else None,
+                                                    ctypes.byref(opts), self.p, _lib.ptr(bs),
+                                                    ctypes.byref(handle), None),
                        "pars3_plan_create")
         self._handle = handle
         self._L = L
@@ -251,9 +266,13 @@ def operator_for_split(s, p=1, block_start=None, device=None, options=None) -> P
     cache = _cache(s)
     op = cache.get(key)
     if op is None:
+        # prepare_gpu(..., keep_device=True) leaves the split on the device: the first
+        # plan takes it (no second upload) and releases it
+        resident = cache.pop("resident_split", None)
         op = Pars3Operator(s.n, s.beta, s.diag, s.mid_ptr, s.mid_col, s.mid_val, s.outer_row,
                            s.outer_col, s.outer_val, p=p, block_start=block_start, device=device,
-                           options=options)
+                           options=options, resident=resident)
+        del resident
         cache[key] = op
     return op
 

@@ -120,11 +120,14 @@ def classify_conflicts_gpu(s, boundaries, device="cuda"):
     return plan, conflict_report(s, plan)
 
 
-def prepare_gpu(m0: SssMatrix, beta: int | None = None, device="cuda", boundaries=None):
+def prepare_gpu(m0: SssMatrix, beta: int | None = None, device="cuda", boundaries=None, keep_device=False):
     """(perm, m, s, bandwidth) of the host chain, computed on the GPU.  With
     ``boundaries`` (a block partition, e.g. ``partition_rows(n, p)``) the
     conflict classification runs on the device-resident split as well and
-    the result is (perm, m, s, bandwidth, plan)."""
+    the result is (perm, m, s, bandwidth, plan).  ``keep_device``: the split's
+    device copies stay attached to ``s`` until its first device plan is built
+    (``prepare`` / ``spmv_pars3``), which then skips the upload of the split
+    (pars3_plan_create_resident)."""
     from .device import require_cuda
     torch = require_cuda()
     dev = torch.device(device)
@@ -179,6 +182,10 @@ def prepare_gpu(m0: SssMatrix, beta: int | None = None, device="cuda", boundarie
     perm = Permutation(h["fw"])
     m = SssMatrix._trusted(n, h["rp"], h["ci"], h["od"], h["dg"])
     s = BandSplit(n, int(beta), h["dg"], h["mp"], h["mc"], h["mv"], h["orow"], h["ocol"], h["oval"])
+    if keep_device:
+        from .device import _cache
+        _cache(s)["resident_split"] = dict(mid_ptr=mp, mid_col=mc, mid_val=mv, outer_row=orow,
+                                           outer_col=ocol, outer_val=oval)
     if boundaries is not None:
         return perm, m, s, bw, plan
     return perm, m, s, bw
