@@ -68,6 +68,8 @@ struct HostPlan {
     int32_t list_tiles = 0;
     int32_t max_local = 0;
     int32_t max_terms = 0;              // most accumulator terms one slot takes in one tile
+    int64_t dmax = 0;                   // most terms one y element sums (row entries + column mirrors
+                                        // + diagonal), when the builder counted them (0: not counted)
 };
 
 // Build from host split arrays (BandSplit layout, split.py:58-113).

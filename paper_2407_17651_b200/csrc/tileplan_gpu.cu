@@ -740,6 +740,24 @@ __global__ void __launch_bounds__(kT) k_materialise(Split S, Opts o, int64_t nt,
     }
 }
 
+// terms per y element: its row's entries, its column's mirrors, its diagonal
+// (the grid form's headroom, tiles.cu grid_data)
+__global__ void k_terms_rows(Split S, int32_t *terms) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < S.n; r += (int64_t)gridDim.x * blockDim.x)
+        terms[r] = 1 + (int32_t)row_count(S, r);
+}
+__global__ void k_terms_cols(int64_t m, const int32_t *col, int32_t *terms) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&terms[col[k]], 1);
+}
+__global__ void k_max_i32(int64_t n, const int32_t *a, int32_t *out) {
+    int32_t best = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        best = max(best, a[i]);
+    best = __reduce_max_sync(0xffffffffu, best);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
 template <class T>
 struct Buf {
     T *p = nullptr;
@@ -793,6 +811,7 @@ int build_tile_plan_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid
         o.seg_max > 8 || o.gap < 2 /* (smaller gaps: alignment can merge runs) */ || o.gap > 20 || o.local_slots > 4094 || o.local_slots < 64 ||
         o.max_segments > 32 * PARS3_GPU_MAX_SLICES || o.sink == kNoSlot || o.sink < o.local_slots)
         return PARS3_OK;
+    int64_t P_dmax = 0;
     const bool verbose = getenv("PARS3_VERBOSE") != nullptr;
     double t_prev = omp_get_wtime();
     auto lap = [&](const char *what) {
@@ -914,6 +933,21 @@ int build_tile_plan_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid
         RC(cudaGetLastError());
     }
     lap("materialise");
+    {  // the most terms one y element sums (HostPlan::dmax)
+        Buf<int32_t> terms, best;
+        RC(terms.alloc(n));
+        RC(best.alloc(1));
+        RC(cudaMemset(best.p, 0, sizeof(int32_t)));
+        const int G = (int)std::min<int64_t>((n + kT - 1) / kT, 148 * 32);
+        k_terms_rows<<<G, kT>>>(S, terms.p);
+        if (nm > 0) k_terms_cols<<<148 * 32, kT>>>(nm, S.mcol, terms.p);
+        if (outer_count > 0) k_terms_cols<<<148 * 32, kT>>>(outer_count, S.ocol, terms.p);
+        k_max_i32<<<G, kT>>>(n, terms.p, best.p);
+        RC(cudaGetLastError());
+        int32_t hb = 0;
+        RC(cudaMemcpy(&hb, best.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        P_dmax = hb;
+    }
     const int64_t end16 = nv / 16;
     RC(cudaMemcpy(slice_off.p + ns, &end16, sizeof(int64_t), cudaMemcpyHostToDevice));
     Totals ht{};
@@ -928,6 +962,7 @@ int build_tile_plan_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid
     P.slots = (int64_t)ht.slots;
     P.max_nslots = ht.max_nslots;
     P.max_terms = ht.max_terms;
+    P.dmax = P_dmax;
     P.ucol.resize(nu);
     if (nu > 0) RC(cudaMemcpy(P.ucol.data(), ucol.p, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost));
     P.list_tiles = 0;

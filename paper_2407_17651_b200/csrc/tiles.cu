@@ -187,6 +187,11 @@ struct DevPlan {
     int32_t hgrid;  // ceil(log2(most terms one y element sums))
     int32_t cmax;   // most tiles delivering to one row block (grid roundings per element)
     int32_t strict; // this product's scale from its own x (k_xmax pre-pass), not the previous one's
+    // two accumulators in turn: while a product reduces into yacc, each tile
+    // clears its own rows of the other one (read by the previous product's
+    // k_conv, used by the next product), so k_conv writes no zeros: its 8 n
+    // bytes of stores move into the tile kernel, where DRAM has headroom
+    long long *yclear;  // nullptr: one accumulator, cleared by k_conv
 };
 
 
@@ -722,6 +727,8 @@ __device__ __forceinline__ void tile_loop(const DevPlan &P, const double *__rest
                 DCHECK(c >= 0 && c < P.n);
                 if (V != 0) red_add_u64(P.yacc + c, V);
             };
+            if (P.yclear)  // (every row is some tile's own row)
+                for (int i = r0 + tid; i < r1; i += kThreads) __stcs(P.yclear + i, 0ll);
             if (u0 >= 0) {
                 const int32_t *uc = P.ucol + u0;
                 for (int i = tid; i < local; i += kThreads) deliver(i, __ldg(uc + i));
@@ -858,7 +865,7 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(DevPlan P, double *__rest
             for (int u = 0; u < U; u++) {
                 const int64_t j = i + u * stride;
                 if (j < n2) {
-                    __stcs(a2 + j, make_longlong2(0, 0));
+                    if (!P.yclear) __stcs(a2 + j, make_longlong2(0, 0));
                     const double2 v = make_double2((double)Y[u].x * gunit, (double)Y[u].y * gunit);
                     __stcs(y2 + j, v);
                     if (dot) {
@@ -871,7 +878,7 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(DevPlan P, double *__rest
         }
         if ((n & 1) && i0 == 0) {
             const long long Y = P.yacc[n - 1];
-            P.yacc[n - 1] = 0;
+            if (!P.yclear) P.yacc[n - 1] = 0;
             const double v = (double)Y * gunit;
             y[n - 1] = v;
             if (dot) d = fma(v, self ? v : w[n - 1], d);
@@ -880,7 +887,7 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(DevPlan P, double *__rest
     } else {
         for (int64_t i = i0; i < n; i += stride) {
             const long long Y = P.yacc[i];
-            P.yacc[i] = 0;
+            if (!P.yclear) P.yacc[i] = 0;
             const double v = (double)Y * gunit;
             y[i] = v;
             if (dot) d = fma(v, self ? v : w[i], d);
@@ -1288,7 +1295,8 @@ struct pars3_plan {
     // grid form (deterministic single-GPU products)
     int32_t grid_ok = 0, xe_ready = 0, ev_g = 0, hgrid = 0, cmax = 0;
     double *blk_dot = nullptr, *blk_max = nullptr, *part = nullptr;
-    long long *yacc = nullptr;
+    long long *yacc = nullptr, *yacc2 = nullptr;  // (yacc2: the second accumulator, PARS3 two-buffer form)
+    int32_t acc_turn = 0;
     int32_t seen_fp64_tiles = 0, seen_redone = 0;  // pars3_plan_status: counters at its last call
     cudaEvent_t *prof = nullptr;  // pars3_plan_profile: events at the product's phase boundaries
     int prof_k = 0;
@@ -1308,7 +1316,7 @@ struct pars3_plan {
     ~pars3_plan() {
         void *ptrs[] = {tiles, wins, slice_off, rec,    ucol,    diag, gs,   phase_clk, perm,
                         iperm, xs,   ys,        ccol,   cval,    clrow, clflags, span_row, span_w0,
-                        span_w1, whead, wtail, yacc_tmp, blk_dot, blk_max, part, yacc};
+                        span_w1, whead, wtail, yacc_tmp, blk_dot, blk_max, part, yacc, yacc2};
         for (void *q : ptrs)
             if (q) cudaFree(q);
     }
@@ -1385,29 +1393,31 @@ static int grid_data(const pars3_split_view *v, const HostPlan &hp, GridData &G)
         G.ev_g = std::max(G.ev_g, hp.tiles[t].ev);
     }
     // terms per y element: row entries + column mirrors + the diagonal
-    std::vector<int32_t> terms(n, 1);
-    const int64_t nm = v->mid_ptr ? v->mid_ptr[n] : 0;
-#pragma omp parallel for schedule(static)
-    for (int64_t r = 0; r < n; r++) terms[r] += (int32_t)(v->mid_ptr[r + 1] - v->mid_ptr[r]);
-#pragma omp parallel for schedule(static)
-    for (int64_t k = 0; k < nm; k++) {
-#pragma omp atomic
-        terms[v->mid_col[k]]++;
-    }
-#pragma omp parallel for schedule(static)
-    for (int64_t k = 0; k < v->outer_count; k++) {
-#pragma omp atomic
-        terms[v->outer_row[k]]++;
-#pragma omp atomic
-        terms[v->outer_col[k]]++;
-    }
-    int64_t dmax = 1;
+    // (counted by the device builder when it built the plan)
+    int64_t dmax = std::max<int64_t>(1, hp.dmax);
     double dg = 0.0;
-#pragma omp parallel for schedule(static) reduction(max : dmax, dg)
-    for (int64_t r = 0; r < n; r++) {
-        dmax = std::max<int64_t>(dmax, terms[r]);
-        dg = std::max(dg, std::fabs(v->diag[r]));
+    if (hp.dmax <= 0) {
+        std::vector<int32_t> terms(n, 1);
+        const int64_t nm = v->mid_ptr ? v->mid_ptr[n] : 0;
+#pragma omp parallel for schedule(static)
+        for (int64_t r = 0; r < n; r++) terms[r] += (int32_t)(v->mid_ptr[r + 1] - v->mid_ptr[r]);
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < nm; k++) {
+#pragma omp atomic
+            terms[v->mid_col[k]]++;
+        }
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < v->outer_count; k++) {
+#pragma omp atomic
+            terms[v->outer_row[k]]++;
+#pragma omp atomic
+            terms[v->outer_col[k]]++;
+        }
+#pragma omp parallel for schedule(static) reduction(max : dmax)
+        for (int64_t r = 0; r < n; r++) dmax = std::max<int64_t>(dmax, terms[r]);
     }
+#pragma omp parallel for schedule(static) reduction(max : dg)
+    for (int64_t r = 0; r < n; r++) dg = std::max(dg, std::fabs(v->diag[r]));
     while ((1ll << G.hgrid) < dmax) G.hgrid++;
     if (dg > 0.0) {
         int e = 0;
@@ -1443,6 +1453,15 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
         if (opt->gap >= 0) o0.gap = opt->gap;
         if (opt->mode > 0) o0.mode = opt->mode;
         o0.skip_empty = (opt->flags & PARS3_PLAN_SKIP_EMPTY) != 0;
+        if (o0.skip_empty) {
+            // a skipped row has no slot, so it could not take its diagonal term
+            // (and a list tile's own rows would no longer be the tail of its
+            // column list): SKIP_EMPTY plans carry no diagonal
+            for (int64_t i = 0; i < s->n; i++)
+                if (s->diag[i] != 0.0)
+                    PARS3_FAIL(PARS3_ERR_ARG, "PARS3_PLAN_SKIP_EMPTY needs an all-zero diagonal (row %lld has %g)",
+                               (long long)i, s->diag[i]);
+        }
         if ((opt->flags & PARS3_PLAN_CUT_BLOCKS) && block_start && p > 1)
             for (int32_t r = 1; r < p; r++) o0.cuts.push_back((int32_t)block_start[r]);
         if (opt->max_ctas > 0) max_ctas = opt->max_ctas;
@@ -1728,6 +1747,8 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
         ZALLOC(blk_dot, std::max<int64_t>(pl->ntiles, kConvGrid));
         ZALLOC(blk_max, std::max<int64_t>(pl->ntiles, kConvGrid));
         ZALLOC(yacc, pl->n);
+        const char *tb = getenv("PARS3_TWO_ACC");  // A/B knob
+        if (!(tb && tb[0] == '0')) ZALLOC(yacc2, pl->n);
     }
 #undef UP
 #undef ZALLOC
@@ -1832,6 +1853,11 @@ static int launch_red(pars3_plan *pl, const double *x, double *y, bool acc, cuda
 static int launch_grid(pars3_plan *pl, const double *x, double *y, const double *w, double *dot,
                        bool dot_self, bool strict, cudaStream_t st) {
     DevPlan P = dev_plan(pl);
+    if (pl->yacc2) {  // this product's accumulator, and the one its tiles clear
+        P.yacc = pl->acc_turn ? pl->yacc2 : pl->yacc;
+        P.yclear = pl->acc_turn ? pl->yacc : pl->yacc2;
+        pl->acc_turn ^= 1;
+    }
     if (strict || !pl->xe_ready) {  // the scale bound from a pass over this x
         CUDA_TRY(cudaMemsetAsync(&pl->gs->xe_pre, 0, sizeof(int32_t), st));
         const int grid = (int)std::min<int64_t>(148 * 4, (pl->n + 511) / 512);
