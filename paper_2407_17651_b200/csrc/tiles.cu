@@ -836,9 +836,13 @@ __device__ __forceinline__ void grid_sync(GState *g) {
 // that finishes last sums the shares in CTA order, runs the accuracy check
 // (the grid's rounding against ||y||_inf) and sets the next product's scale
 // bound.  No shared memory, many CTAs, eight pairs in flight per thread.
+#ifndef PARS3_CONV_U  // tuning builds
+#define PARS3_CONV_U 8
+#define PARS3_CONV_MINB 2
+#endif
 constexpr int kConvThreads = 256;
-constexpr int kConvGrid = 148 * 8;
-__global__ void __launch_bounds__(kConvThreads) k_conv(DevPlan P, double *__restrict__ y, const double *w,
+constexpr int kConvGrid = 148 * 8;  // (the most CTAs; the launch uses one resident wave)
+__global__ void __launch_bounds__(kConvThreads, PARS3_CONV_MINB) k_conv(DevPlan P, double *__restrict__ y, const double *w,
                                                        double *dot, int dot_self, int32_t n) {
     __shared__ double s_red[kConvThreads / 32];
     __shared__ int s_last;
@@ -855,7 +859,7 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(DevPlan P, double *__rest
         longlong2 *a2 = reinterpret_cast<longlong2 *>(P.yacc);
         double2 *y2 = reinterpret_cast<double2 *>(y);
         const double2 *w2 = reinterpret_cast<const double2 *>(w);
-        constexpr int U = 8;
+        constexpr int U = PARS3_CONV_U;
         for (int64_t i = i0; i < n2; i += U * stride) {
             longlong2 Y[U];
 #pragma unroll
@@ -1278,7 +1282,7 @@ struct pars3_plan {
     int32_t p = 1;
     int32_t ntiles = 0, nslices = 0, lmax = 0;
     int64_t nnz = 0, slots = 0, nwins = 0;
-    int grid = 0, grid_redo = 0;
+    int grid = 0, grid_redo = 0, conv_grid = 0;
     size_t smem = 0;
     TileMeta *tiles = nullptr;
     Window *wins = nullptr;
@@ -1787,6 +1791,14 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
     if (max_ctas > 0 && pl->grid > max_ctas) pl->grid = max_ctas;
     if (pl->grid > pl->ntiles) pl->grid = pl->ntiles > 0 ? pl->ntiles : 1;
     pl->grid_redo = std::min(pl->grid, per_sm_redo * sms);
+    {  // k_conv: one resident wave (measured: 1 184 CTAs in four waves 58 us, one wave of 296 52 us on c5)
+        int per_sm_conv = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_conv, k_conv, kConvThreads, 0) != cudaSuccess ||
+            per_sm_conv < 1)
+            per_sm_conv = 1;
+        pl->conv_grid = std::min(kConvGrid, per_sm_conv * sms);
+        if (const char *e = getenv("PARS3_CONV_GRID")) pl->conv_grid = std::max(1, std::min(kConvGrid, atoi(e)));
+    }
     lap("upload");
     *out = pl;
     return PARS3_OK;
@@ -1876,7 +1888,7 @@ static int launch_grid(pars3_plan *pl, const double *x, double *y, const double 
     LAUNCH_CHECK();
     mark(pl, st);
     int32_t n32 = (int32_t)pl->n;
-    k_conv<<<kConvGrid, kConvThreads, 0, st>>>(P, y, w, dot, ds, n32);
+    k_conv<<<pl->conv_grid, kConvThreads, 0, st>>>(P, y, w, dot, ds, n32);
     LAUNCH_CHECK();
     void *args[] = {(void *)&P, (void *)&x, (void *)&y, (void *)&w, (void *)&dot, (void *)&ds, (void *)&n32};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_finish, dim3(pl->grid_redo), dim3(kThreads), args,

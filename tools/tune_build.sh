@@ -8,7 +8,7 @@ d=paper_2407_17651_b200/_build/tune_$name
 mkdir -p $d
 cd paper_2407_17651_b200/csrc
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp"
-D="-DPARS3_THREADS=$thr -DPARS3_MIN_BLOCKS=$mb -DPARS3_CAP=$cap -DPARS3_MAX_SLICES=$ms"
+D="-DPARS3_THREADS=$thr -DPARS3_MIN_BLOCKS=$mb -DPARS3_CAP=$cap -DPARS3_MAX_SLICES=$ms ${EXTRA_DEFS:-}"
 objs=""
 for f in *.cu; do nvcc $F $D -Xptxas -v -c -o ../_build/tune_$name/${f%.cu}.o $f 2> ../_build/tune_$name/${f%.cu}.ptxas.txt; objs="$objs ../_build/tune_$name/${f%.cu}.o"; done
 for f in *.cpp; do g++ -O3 -fPIC -fopenmp -std=c++17 $D -c -o ../_build/tune_$name/${f%.cpp}.cpp.o $f; objs="$objs ../_build/tune_$name/${f%.cpp}.cpp.o"; done
