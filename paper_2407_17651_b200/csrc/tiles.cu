@@ -1577,6 +1577,7 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
     if (may_permute && (unstructured || (flags & PARS3_PLAN_LOCALITY)) && hp.nnz > 0) {
         rc = pars3::locality_order(s, lo);
         if (rc) return rc;
+        lap("locality order");
         pars3_split_view v{s->n, s->beta, lo.diag.data(), lo.row_ptr.data(), lo.col.data(),
                            lo.val.data(), 0, nullptr, nullptr, nullptr};
         PlanOptions o2;
@@ -1584,6 +1585,7 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
         HostPlan hp2;
         rc = build(&v, o2, words2, hp2, nullptr);
         if (rc) return rc;
+        lap("tile plan, locality order");
         const int64_t local2 = local_of(hp2);
         if (10 * local2 < 7 * local) {
             dp.release();
@@ -1669,12 +1671,18 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
     }
     pl->local_slots = local;
     pl->dropped = lo.dropped;
-    std::vector<double> diag = lo.forward.empty() ? std::vector<double>(s->diag, s->diag + s->n)
-                                                  : std::move(lo.diag);
-    pl->diag_const = 1;
-    pl->diag_alpha = s->n ? diag[0] : 0.0;
-    for (int64_t i = 1; i < s->n && pl->diag_const; i++)
-        if (diag[i] != diag[0]) pl->diag_const = 0;
+    // (a constant diagonal, strict or shifted skew, is not uploaded)
+    const double *dsrc = lo.forward.empty() ? s->diag : lo.diag.data();
+    pl->diag_alpha = s->n ? dsrc[0] : 0.0;
+    {
+        int varies = 0;
+        const double d0 = pl->diag_alpha;
+#pragma omp parallel for schedule(static) reduction(| : varies)
+        for (int64_t i = 0; i < s->n; i++) varies |= dsrc[i] != d0;
+        pl->diag_const = !varies;
+    }
+    std::vector<double> diag;
+    if (!pl->diag_const) diag.assign(dsrc, dsrc + s->n);
 #define UP(dst, src)                               \
     do {                                           \
         int _r = upload(&pl->dst, src);            \
