@@ -1158,19 +1158,18 @@ __global__ void __launch_bounds__(256, 2) k_csr(int32_t nrows, int64_t ne, int64
     const int lane = threadIdx.x & 31;
     const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < nwarps; w += wstride) {
+        // lane l holds the CSR entries e0 .. e0 + K - 1; the plan stores them
+        // lane-interleaved (entry k of lane l at w * 512 + k * 32 + l), so
+        // every load below is one coalesced 128 / 256-byte access per warp
+        // (lane-contiguous storage cost 32 L1 wavefronts per load: 43 % of
+        // the kernel's L1TEX cycles)
         const int64_t L = w * 32 + lane, e0 = L * K;
         int32_t c[K];
         double v[K], xc[K];
-        const int4 *c4 = reinterpret_cast<const int4 *>(col + e0);
-        const double2 *v2 = reinterpret_cast<const double2 *>(val + e0);
+        const int32_t *cw = col + w * (32 * K) + lane;
+        const double *vw = val + w * (32 * K) + lane;
 #pragma unroll
-        for (int h = 0; h < K / 4; h++) {
-            const int4 a = __ldcs(c4 + h);
-            c[4 * h] = a.x;
-            c[4 * h + 1] = a.y;
-            c[4 * h + 2] = a.z;
-            c[4 * h + 3] = a.w;
-        }
+        for (int k = 0; k < K; k++) c[k] = __ldcs(cw + 32 * k);
         const int32_t row0 = __ldcs(lane_row + L);
         const uint32_t fl = __ldcs(lane_flags + L);
 #pragma unroll
@@ -1179,11 +1178,7 @@ __global__ void __launch_bounds__(256, 2) k_csr(int32_t nrows, int64_t ne, int64
             xc[k] = e0 + k < ne ? __ldg(x + c[k]) : 0.0;  // all in flight
         }
 #pragma unroll
-        for (int h = 0; h < K / 2; h++) {
-            const double2 a = __ldcs(v2 + h);
-            v[2 * h] = a.x;
-            v[2 * h + 1] = a.y;
-        }
+        for (int k = 0; k < K; k++) v[k] = __ldcs(vw + 32 * k);
         // the lane's row segments, in order
         const bool cont = !(fl & 1u);  // the first entry continues a row of an earlier lane
         bool first = true;
@@ -1702,6 +1697,22 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
         pl->bytes += (int64_t)_b;                                                             \
     } while (0)
     if (direct) {
+        {  // lane-interleaved storage within each warp of 512 entries (k_csr)
+            const int64_t nw = (int64_t)F.col.size() / pars3::kCsrWarp;
+            std::vector<int32_t> c2(F.col.size());
+            std::vector<double> v2(F.val.size());
+#pragma omp parallel for schedule(static)
+            for (int64_t w = 0; w < nw; w++)
+                for (int l = 0; l < 32; l++)
+                    for (int k = 0; k < pars3::kCsrLane; k++) {
+                        const int64_t src = w * pars3::kCsrWarp + l * pars3::kCsrLane + k;
+                        const int64_t dst = w * pars3::kCsrWarp + k * 32 + l;
+                        c2[dst] = F.col[src];
+                        v2[dst] = F.val[src];
+                    }
+            F.col.swap(c2);
+            F.val.swap(v2);
+        }
         pl->direct = 1;
         pl->ne = F.ne;
         pl->nwarps = (int64_t)F.col.size() / pars3::kCsrWarp;
