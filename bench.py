@@ -586,7 +586,17 @@ def run_gpu(args):
                                  "(k_finish: the grid accumulator -> fp64 y; or the row fix-up); achieved = "
                                  "algorithmic bytes / their time together" if world == 1 else
                                  "each rank's local product"),
-                     "phases_ms": phases},
+                     "phases_ms": phases,
+                     # the dominant kernel alone (the prompt's definition: algorithmic bytes of
+                     # one launch / that kernel's average duration, CUDA events on its stream)
+                     "dominant_kernel": ({
+                         "name": ("k_csr (full CSR, row-major form)" if stats.get("direct") else
+                                  "k_tiles (+ the locality gather of x)" if stats.get("locality_order")
+                                  else "k_tiles"),
+                         "ms": phases["main_ms"],
+                         "achieved": B_rank / (phases["main_ms"] * 1e-3) / 1e9,
+                         "frac": B_rank / (phases["main_ms"] * 1e-3) / 1e9 / peak}
+                         if phases and phases.get("main_ms", 0) > 0 else None)},
         "cpu_baseline": cpu,
         "e2e": {"value": B / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms,

@@ -230,12 +230,13 @@ int pars3_plan_kernel_count(const pars3_plan *plan, int32_t with_dot, int32_t *c
 /* Device bytes held by the plan. */
 int pars3_plan_bytes(const pars3_plan *plan, int64_t *bytes);
 
-/* stats[19] = {tiles, slices, padded slots, stored entries, windows,
+/* stats[20] = {tiles, slices, padded slots, stored entries, windows,
  * max local slots, grid CTAs, device bytes, list-mode tiles, accumulator
  * words (0 = fp64, 2 or 3 = fixed point), locality order (0/1), shared-memory
  * slots over all tiles, edges the locality filter dropped, direct mode (0/1),
  * grid form (0/1), grid headroom bits, grid deliveries per row block, grid
- * value exponent, tile plan built on the device (0/1)}. */
+ * value exponent, tile plan built on the device (0/1), far entries kept out
+ * of the tiles}. */
 int pars3_plan_stats(const pars3_plan *plan, int64_t *stats);
 
 /* Inspection / tests: the tile plan of a split as host arrays,

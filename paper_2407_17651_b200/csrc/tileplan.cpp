@@ -218,13 +218,37 @@ void draft_range(const Rows &R, int32_t a, int32_t b, const PlanOptions &o,
     d.r1 = b;
     make_windows(scratch, o.gap, true, R.n, d);
     cut_windows(o.cuts, d);
-    // too fragmented for windows: the tile will carry an explicit column
-    // list, so do not pay for gap or alignment slots (the rebuilt windows
-    // are cut again: a tile that ends up with <= kMaxWindows of them stays
-    // in window mode, and no window may straddle a rank boundary)
     if ((int)d.wlo.size() > kMaxWindows) {
-        make_windows(scratch, 0, false, R.n, d);
-        cut_windows(o.cuts, d);
+        // Too fragmented for gap-merged windows.  When the whole column span
+        // [smallest column, b) fits the local space, one dense window over it
+        // keeps the tile in window mode (TMA copies of x, coalesced
+        // deliveries; a band's sparse fringe, the first rows of a stencil);
+        // when halving the range would make it fit, halve instead of
+        // carrying a column list.  (make_windows left scratch sorted.)
+        Draft one;
+        one.r0 = a;
+        one.r1 = b;
+        int32_t lo = scratch.empty() ? a : (scratch[0] & ~1), hi = b;
+        if ((hi & 1) && hi < R.n) hi++;
+        one.wlo.push_back(lo);
+        one.wlen.push_back(hi - lo);
+        one.local = hi - lo;
+        cut_windows(o.cuts, one);
+        if (one.local <= o.local_slots && (int)one.wlo.size() <= kMaxWindows) {
+            d = std::move(one);
+        } else if (b - a > 64 && one.local - (b - a) / 2 <= o.local_slots) {
+            const int32_t mid = a + (((b - a) / 2 + 31) & ~31);
+            draft_range(R, a, mid, o, out, scratch);
+            draft_range(R, mid, b, o, out, scratch);
+            return;
+        } else {
+            // an explicit column list: do not pay for gap or alignment slots
+            // (the rebuilt windows are cut again: a tile that ends up with <=
+            // kMaxWindows of them stays in window mode, and no window may
+            // straddle a rank boundary)
+            make_windows(scratch, 0, false, R.n, d);
+            cut_windows(o.cuts, d);
+        }
     }
     if (d.local <= o.local_slots && !chunk_row) {
         out.push_back(std::move(d));

@@ -265,13 +265,25 @@ __global__ void __launch_bounds__(kT) k_draft(Split S, Opts o, int64_t nranges, 
                     act = 3;
                     s_why |= 2;
                 }
-                const int nw = s_ns;
-                bool as_list = false;
+                int nw = s_ns;
+                bool as_list = false, one_window = false;
                 if (act == 0 && (nw > kMaxWindows || nw != s_ne)) {
-                    // too fragmented for windows: the host rebuilds them without gap
-                    // or alignment slots (local = the distinct columns) and keeps the
-                    // range as a list-mode tile if that fits, else halves it
-                    if (s_distinct <= o.local_slots) {
+                    // too fragmented for gap-merged windows (draft_range, tileplan.cpp):
+                    // one dense window over the whole column span when it fits; else
+                    // halve when that would make it fit; else the host rebuilds the
+                    // windows without gap or alignment slots (local = the distinct
+                    // columns) and keeps a list-mode tile if that fits, else halves
+                    int32_t lo = cmin & ~1, hi = b;
+                    if ((hi & 1) && hi < S.n) hi++;
+                    if (hi - lo <= o.local_slots) {
+                        one_window = true;
+                        nw = 1;
+                        s_ns = s_ne = 1;
+                        s_starts[0] = lo;
+                        s_ends[0] = b;
+                    } else if (b - a > 64 && (hi - lo) - (b - a) / 2 <= o.local_slots) {
+                        act = 2;
+                    } else if (s_distinct <= o.local_slots) {
                         as_list = true;
                     } else if (b - a > 1) {
                         act = 2;
@@ -280,6 +292,7 @@ __global__ void __launch_bounds__(kT) k_draft(Split S, Opts o, int64_t nranges, 
                         s_why |= 16;
                     }
                 }
+                (void)one_window;
                 if (act == 0 && as_list) {
                     DraftTile d;
                     d.a = a;

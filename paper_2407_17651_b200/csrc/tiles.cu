@@ -192,6 +192,11 @@ struct DevPlan {
     // k_conv, used by the next product), so k_conv writes no zeros: its 8 n
     // bytes of stores move into the tile kernel, where DRAM has headroom
     long long *yclear;  // nullptr: one accumulator, cleared by k_conv
+    // far entries (k_far_*): the few long-range entries of a locality-ordered
+    // plan, kept out of the tiles so that those stay in window mode
+    const int32_t *far_row, *far_col;
+    const double *far_val;
+    int32_t nfar;
 };
 
 
@@ -986,6 +991,12 @@ k_finish(DevPlan P, const double *__restrict__ x, double *__restrict__ y, const 
     for (int64_t i = i0; i < n; i += stride) y[i] = 0.0;
     grid_sync(g);
     tile_loop<0, false, false>(P, x, y, nullptr, nullptr, false, &g->claim2);  // fp64 accumulators
+    for (int64_t e = i0; e < P.nfar; e += stride) {  // the far part
+        const int32_t i = P.far_row[e], c = P.far_col[e];
+        const double v = P.far_val[e];
+        atomicAdd(y + i, v * x[c]);
+        atomicAdd(y + c, -v * x[i]);
+    }
     grid_sync(g);
     if (dot) {  // per-CTA shares in blk_dot (>= kDotGrid entries), summed in CTA order
         double d = 0.0;
@@ -1010,6 +1021,38 @@ k_finish(DevPlan P, const double *__restrict__ x, double *__restrict__ y, const 
             g->redone++;
             __threadfence();
         }
+    }
+}
+
+// The far part of a plan (the outer part's long-range entries: the north
+// star's separate gather / scatter pass): entry (i, c, v) adds v x_c to y_i
+// and -v x_i to y_c (serial.py:56-59).  GRID form: each term goes onto the
+// product's fixed-point grid and is reduced into yacc as an integer, so the
+// sum does not depend on the order (bitwise repeatable); the terms count
+// among the grid's roundings (cmax) and headroom (hgrid).  x needs no check
+// here: every row is some tile's own row, whose x the tile kernel scanned.
+__global__ void __launch_bounds__(256) k_far_grid(DevPlan P, const double *__restrict__ x) {
+    const int xe = product_xe(P);
+    const int Eg = max(-960, min(960, P.ev_g + xe + P.hgrid));
+    const double gscale = ldexp(1.0, 62 - Eg);
+    const int32_t stride = gridDim.x * blockDim.x;
+    for (int32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < P.nfar; e += stride) {
+        const int32_t i = __ldcs(P.far_row + e), c = __ldcs(P.far_col + e);
+        const double v = __ldcs(P.far_val + e);
+        DCHECK(i >= 0 && i < P.n && c >= 0 && c < P.n);
+        const long long a = __double2ll_rn(v * __ldg(x + c) * gscale), b = __double2ll_rn(-v * __ldg(x + i) * gscale);
+        if (a) red_add_u64(P.yacc + i, a);
+        if (b) red_add_u64(P.yacc + c, b);
+    }
+}
+// RED form (y += A x, plans without the grid form): fp64 reductions
+__global__ void __launch_bounds__(256) k_far_red(DevPlan P, const double *__restrict__ x, double *y) {
+    const int32_t stride = gridDim.x * blockDim.x;
+    for (int32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < P.nfar; e += stride) {
+        const int32_t i = __ldcs(P.far_row + e), c = __ldcs(P.far_col + e);
+        const double v = __ldcs(P.far_val + e);
+        atomicAdd(y + i, v * __ldg(x + c));
+        atomicAdd(y + c, -v * __ldg(x + i));
     }
 }
 
@@ -1306,6 +1349,9 @@ struct pars3_plan {
     int64_t local_slots = 0, dropped = 0;
     // row-major form (k_csr): the full CSR of A in lanes of 16 entries, no tiles
     int32_t built_on_device = 0;  // the tile plan came from tileplan_gpu.cu
+    int32_t nfar = 0;             // far entries kept out of the tiles (k_far_grid / k_far_red)
+    int32_t *far_row = nullptr, *far_col = nullptr;
+    double *far_val = nullptr;
     int32_t direct = 0, nspan = 0;
     int64_t ne = 0, nwarps = 0;
     int32_t *ccol = nullptr, *clrow = nullptr, *span_row = nullptr, *span_w0 = nullptr, *span_w1 = nullptr;
@@ -1315,7 +1361,7 @@ struct pars3_plan {
     ~pars3_plan() {
         void *ptrs[] = {tiles, wins, slice_off, rec,    ucol,    diag, gs,   phase_clk, perm,
                         iperm, xs,   ys,        ccol,   cval,    clrow, clflags, span_row, span_w0,
-                        span_w1, whead, wtail, yacc_tmp, blk_dot, blk_max, part, yacc, yacc2};
+                        span_w1, whead, wtail, yacc_tmp, blk_dot, blk_max, part, yacc, yacc2, far_row, far_col, far_val};
         for (void *q : ptrs)
             if (q) cudaFree(q);
     }
@@ -1347,7 +1393,10 @@ struct GridData {
     int32_t hgrid = 0, cmax = 0, ev_g = -1074;
 };
 
-static int grid_data(const pars3_split_view *v, const HostPlan &hp, GridData &G) {
+// (far_terms / far_vmax: the far part's most terms on one row and its largest
+// |value|: they join the grid's roundings, headroom and value bound)
+static int grid_data(const pars3_split_view *v, const HostPlan &hp, GridData &G, int32_t far_terms = 0,
+                     double far_vmax = 0.0) {
     const int64_t n = v->n;
     const int64_t nt = (int64_t)hp.tiles.size();
     std::vector<int32_t> blk(n, -1);
@@ -1417,6 +1466,13 @@ static int grid_data(const pars3_split_view *v, const HostPlan &hp, GridData &G)
     }
 #pragma omp parallel for schedule(static) reduction(max : dg)
     for (int64_t r = 0; r < n; r++) dg = std::max(dg, std::fabs(v->diag[r]));
+    dmax += far_terms;
+    G.cmax += far_terms;
+    if (far_vmax > 0.0) {
+        int e = 0;
+        std::frexp(far_vmax, &e);
+        G.ev_g = std::max(G.ev_g, e);
+    }
     while ((1ll << G.hgrid) < dmax) G.hgrid++;
     if (dg > 0.0) {
         int e = 0;
@@ -1424,6 +1480,72 @@ static int grid_data(const pars3_split_view *v, const HostPlan &hp, GridData &G)
         G.ev_g = std::max(G.ev_g, e);
     }
     return PARS3_OK;
+}
+
+// Far split of a locality-ordered matrix.  In the
+// internal order nearly every entry lies within a couple of thousand labels
+// of the diagonal (c3: 98.5 % within 2 560); the few long-range entries are
+// what forces explicit column lists on the tiles.  Entries farther than T
+// from the diagonal (a prefix of each row: columns ascend) are taken out
+// into the far part (k_far_grid), so that the near part's tiles are dense
+// column windows: TMA copies of x and coalesced deliveries instead of one
+// gather and one reduction per slot.
+struct FarSplit {
+    std::vector<int64_t> nptr;
+    std::vector<int32_t> ncol, frow, fcol;
+    std::vector<double> nval, fval;
+    double fvmax = 0.0;
+    int32_t fterms = 0;  // most far terms on one row
+};
+
+static bool split_far(const LocalityOrder &lo, int64_t n, int32_t T, FarSplit &fs) {
+    const int64_t m = lo.row_ptr[n];
+    std::vector<int64_t> fptr(n + 1, 0);
+    fs.nptr.assign(n + 1, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; i++) {
+        int64_t k = lo.row_ptr[i];
+        while (k < lo.row_ptr[i + 1] && i - lo.col[k] > T) k++;
+        fptr[i + 1] = k - lo.row_ptr[i];
+        fs.nptr[i + 1] = lo.row_ptr[i + 1] - k;
+    }
+    for (int64_t i = 0; i < n; i++) {
+        fptr[i + 1] += fptr[i];
+        fs.nptr[i + 1] += fs.nptr[i];
+    }
+    const int64_t nf = fptr[n];
+    if (nf == 0 || 20 * nf > m || nf >= INT32_MAX) return false;
+    fs.frow.resize(nf);
+    fs.fcol.resize(nf);
+    fs.fval.resize(nf);
+    fs.ncol.resize(m - nf);
+    fs.nval.resize(m - nf);
+    std::vector<int32_t> terms(n, 0);
+    double vmax = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : vmax)
+    for (int64_t i = 0; i < n; i++) {
+        int64_t k = lo.row_ptr[i];
+        for (int64_t f = fptr[i]; f < fptr[i + 1]; f++, k++) {
+            fs.frow[f] = (int32_t)i;
+            fs.fcol[f] = lo.col[k];
+            fs.fval[f] = lo.val[k];
+            vmax = std::max(vmax, std::fabs(lo.val[k]));
+#pragma omp atomic
+            terms[i]++;
+#pragma omp atomic
+            terms[lo.col[k]]++;
+        }
+        for (int64_t q = fs.nptr[i]; q < fs.nptr[i + 1]; q++, k++) {
+            fs.ncol[q] = lo.col[k];
+            fs.nval[q] = lo.val[k];
+        }
+    }
+    int32_t tmax = 0;
+#pragma omp parallel for schedule(static) reduction(max : tmax)
+    for (int64_t i = 0; i < n; i++) tmax = std::max(tmax, terms[i]);
+    fs.fvmax = vmax;
+    fs.fterms = tmax;
+    return true;
 }
 
 extern "C" int pars3_plan_create(const pars3_split_view *s, const pars3_plan_options *opt,
@@ -1566,6 +1688,8 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
     // unstructured list tiles whose slots hold few entries each, kept when
     // it cuts the shared-memory slots (= x gathers + y reductions) by 30 %
     LocalityOrder lo;
+    FarSplit fs;  // the near part's arrays (the tiles' split) and the far part, when used
+    bool far_used = false;
     const bool may_permute =
         !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_NO_LOCALITY | PARS3_PLAN_DIRECT)) && s->n > 1;
     const bool unstructured = 2ll * hp.list_tiles > (int64_t)hp.tiles.size() && 4 * local > hp.nnz;
@@ -1573,28 +1697,66 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
         rc = pars3::locality_order(s, lo);
         if (rc) return rc;
         lap("locality order");
-        pars3_split_view v{s->n, s->beta, lo.diag.data(), lo.row_ptr.data(), lo.col.data(),
-                           lo.val.data(), 0, nullptr, nullptr, nullptr};
-        PlanOptions o2;
-        int words2 = 0;
-        HostPlan hp2;
-        rc = build(&v, o2, words2, hp2, nullptr);
-        if (rc) return rc;
-        lap("tile plan, locality order");
-        const int64_t local2 = local_of(hp2);
-        if (10 * local2 < 7 * local) {
-            dp.release();
-            o = o2;
-            words = words2;
-            hp = std::move(hp2);
-            local = local2;
-        } else {
-            lo = LocalityOrder();
+        // first with the long-range entries taken out (window-mode tiles + the far part) ...
+        const char *nf_env = getenv("PARS3_NO_FAR");  // A/B knob
+        if (!(nf_env && nf_env[0] == '1')) {
+            const int32_t T = std::min(want_local, words0 == 3 ? kLocalFixed : kLocalExact) - 640;
+            if (T >= 256 && split_far(lo, s->n, T, fs)) {
+                pars3_split_view vn{s->n, s->beta, lo.diag.data(), fs.nptr.data(), fs.ncol.data(),
+                                    fs.nval.data(), 0, nullptr, nullptr, nullptr};
+                PlanOptions o2;
+                int words2 = 0;
+                HostPlan hp2;
+                DpGuard dpn;  // (the first plan's device arrays stay until this one is accepted)
+                rc = build(&vn, o2, words2, hp2, &dpn.d);
+                if (rc) return rc;
+                lap("tile plan, near part");
+                const int64_t local2 = local_of(hp2);
+                if (verbose)
+                    fprintf(stderr, "pars3 plan: near part: T %d far %zu tiles %zu list %d slots %lld (was %lld) words %d "
+                                    "max terms %d\n", T, fs.frow.size(), hp2.tiles.size(), hp2.list_tiles,
+                            (long long)local2, (long long)local, words2, hp2.max_terms);
+                if (10ll * hp2.list_tiles <= (int64_t)hp2.tiles.size() && 10 * local2 < 7 * local) {
+                    o = o2;
+                    words = words2;
+                    hp = std::move(hp2);
+                    local = local2;
+                    far_used = true;
+                    dp.release();
+                    dp = dpn.d;
+                    dpn.d = pars3::DevicePlan();
+                }
+            }
+        }
+        // ... else every entry in the tiles
+        if (!far_used) {
+            fs = FarSplit();
+            pars3_split_view v{s->n, s->beta, lo.diag.data(), lo.row_ptr.data(), lo.col.data(),
+                               lo.val.data(), 0, nullptr, nullptr, nullptr};
+            PlanOptions o2;
+            int words2 = 0;
+            HostPlan hp2;
+            rc = build(&v, o2, words2, hp2, nullptr);
+            if (rc) return rc;
+            lap("tile plan, locality order");
+            const int64_t local2 = local_of(hp2);
+            if (10 * local2 < 7 * local) {
+                dp.release();
+                o = o2;
+                words = words2;
+                hp = std::move(hp2);
+                local = local2;
+            } else {
+                lo = LocalityOrder();
+            }
         }
     }
     // the split the tiles were built from (the caller's, or P A P^T)
     pars3_split_view used = *s;
-    if (!lo.forward.empty())
+    if (far_used)
+        used = pars3_split_view{s->n, s->beta, lo.diag.data(), fs.nptr.data(), fs.ncol.data(),
+                                fs.nval.data(), 0, nullptr, nullptr, nullptr};
+    else if (!lo.forward.empty())
         used = pars3_split_view{s->n, s->beta, lo.diag.data(), lo.row_ptr.data(), lo.col.data(),
                                 lo.val.data(), 0, nullptr, nullptr, nullptr};
     // direct mode: the tiles would stage about one entry per slot (no reuse
@@ -1628,7 +1790,7 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
     const bool grid_ok = !direct && !hp.tiles.empty() && safe_values && !o0.skip_empty;
     if (grid_ok) {
         try {
-            rc = grid_data(&used, hp, G);
+            rc = grid_data(&used, hp, G, far_used ? fs.fterms : 0, far_used ? fs.fvmax : 0.0);
         } catch (const std::bad_alloc &) {
             PARS3_FAIL(PARS3_ERR_NOMEM, "out of host memory");
         }
@@ -1742,6 +1904,12 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
         UP(rec, hp.rec);
     }
     UP(ucol, hp.ucol);
+    if (far_used) {
+        pl->nfar = (int32_t)fs.frow.size();
+        UP(far_row, fs.frow);
+        UP(far_col, fs.fcol);
+        UP(far_val, fs.fval);
+    }
     if (!pl->diag_const) UP(diag, diag);
     if (!lo.forward.empty()) {
         UP(perm, lo.forward);
@@ -1847,6 +2015,10 @@ static DevPlan dev_plan(const pars3_plan *pl) {
     P.ev_g = pl->ev_g;
     P.hgrid = pl->hgrid;
     P.cmax = pl->cmax;
+    P.far_row = pl->far_row;
+    P.far_col = pl->far_col;
+    P.far_val = pl->far_val;
+    P.nfar = pl->nfar;
     return P;
 }
 
@@ -1874,6 +2046,10 @@ static int launch_red(pars3_plan *pl, const double *x, double *y, bool acc, cuda
         (peer ? k_tiles<3, true, false> : k_tiles<3, false, false>)<<<pl->grid, kThreads, pl->smem, st>>>(
             P, x, y, nullptr, nullptr, 0);
     LAUNCH_CHECK();
+    if (pl->nfar > 0) {
+        k_far_red<<<std::min(148 * 8, (pl->nfar + 255) / 256), 256, 0, st>>>(P, x, y);
+        LAUNCH_CHECK();
+    }
     mark(pl, st);
     CUDA_TRY(cudaMemsetAsync(&pl->gs->claim, 0, sizeof(int32_t), st));
     return PARS3_OK;
@@ -1905,6 +2081,10 @@ static int launch_grid(pars3_plan *pl, const double *x, double *y, const double 
     else
         k_tiles<3, false, true><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, w, dot, ds);
     LAUNCH_CHECK();
+    if (pl->nfar > 0) {
+        k_far_grid<<<std::min(148 * 8, (pl->nfar + 255) / 256), 256, 0, st>>>(P, x);
+        LAUNCH_CHECK();
+    }
     mark(pl, st);
     int32_t n32 = (int32_t)pl->n;
     k_conv<<<pl->conv_grid, kConvThreads, 0, st>>>(P, y, w, dot, ds, n32);
@@ -2138,7 +2318,7 @@ extern "C" int pars3_plan_kernel_count(const pars3_plan *pl, int32_t with_dot, i
     if (pl->direct) {
         c = (pl->n > 0 ? 1 : 0) + (pl->nspan > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 2 : 0);
     } else if (pl->perm) {
-        c = 2 + (pl->ntiles > 0 ? (grid ? 3 : 1) : 0);
+        c = 2 + (pl->ntiles > 0 ? (grid ? 3 : 1) : 0) + (pl->nfar > 0 ? 1 : 0);
     } else if (grid) {
         c = 3;  // k_tiles, k_conv, k_finish (exits at once unless the product was flagged)
     } else {
@@ -2175,6 +2355,7 @@ extern "C" int pars3_plan_stats(const pars3_plan *pl, int64_t *stats) {
     stats[16] = pl->cmax;
     stats[17] = pl->ev_g;
     stats[18] = pl->built_on_device;
+    stats[19] = pl->nfar;
     return PARS3_OK;
 }
 

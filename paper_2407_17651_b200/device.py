@@ -208,12 +208,12 @@ class Pars3Operator:
         return int(b.value)
 
     def stats(self) -> dict:
-        a = np.zeros(19, dtype=np.int64)
+        a = np.zeros(20, dtype=np.int64)
         _lib.check(self._L.pars3_plan_stats(self._handle, _lib.ptr(a)))
         keys = ("tiles", "slices", "padded_slots", "entries", "windows", "max_local", "grid",
                 "device_bytes", "list_tiles", "accum_words", "locality_order", "local_slots",
                 "locality_dropped", "direct", "grid_form", "grid_hbits", "grid_cmax", "grid_ev",
-                "built_on_device")
+                "built_on_device", "far_entries")
         return {k: int(v) for k, v in zip(keys, a)}
 
     def close(self):

@@ -431,8 +431,26 @@ def test_locality_order(flags, oracle):
         assert abs(float(dot2.item()) - float(x @ yh)) <= 1e-12 * float(np.abs(x) @ np.abs(yh))
         # grid form: tiles + k_conv + k_finish; + perm in/out with a locality
         # order; row-major form: full CSR + span fix-up + dot (two kernels)
-        expect = 5 if st["locality_order"] else 4 if st["direct"] else 3
+        # (one more for the far part: the long-range entries kept out of the tiles)
+        expect = 5 + (1 if st["far_entries"] else 0) if st["locality_order"] else 4 if st["direct"] else 3
         assert op.kernel_count(True) == expect, st
+        if flags == 8 and g.name.startswith("random_band"):
+            # the far part (k_far_grid / k_far_red): window-mode tiles for the band,
+            # bitwise repeatable, IEEE results through the redo as well
+            assert st["far_entries"] > 0 and st["list_tiles"] * 10 <= st["tiles"], st
+            yb = [op.matvec(xd).cpu().numpy().tobytes() for _ in range(5)]
+            assert all(b == yb[0] for b in yb)
+            xi = x.copy()
+            xi[m.n // 3] = np.inf
+            xi[m.n // 2] = 1e300
+            ref_i = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, xi)
+            got_i = op.matvec(torch.from_numpy(xi).cuda()).cpu().numpy()
+            fin = np.isfinite(ref_i)
+            assert np.array_equal(np.isnan(got_i), np.isnan(ref_i))
+            assert np.array_equal(got_i[~fin & ~np.isnan(ref_i)], ref_i[~fin & ~np.isnan(ref_i)])
+            assert rel_err(got_i[fin], ref_i[fin]) <= TOL
+            assert op.status() & 1  # that product was redone in fp64
+            assert rel_err(op.matvec(xd).cpu().numpy(), y_ref) <= TOL
 
 
 @pytest.mark.parametrize("flags", [0, 32, 64])
