@@ -24,6 +24,8 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <new>
 #include <vector>
 
@@ -50,6 +52,13 @@ constexpr int64_t kTwoHopCap = 1 << 14;  // two-hop work per vertex before it co
 
 int locality_order(const pars3_split_view *s, LocalityOrder &out) {
     const int64_t n = s->n;
+    const bool verbose = getenv("PARS3_VERBOSE") != nullptr;  // wall-clock of the stages on stderr
+    double t_prev = omp_get_wtime();
+    auto lap = [&](const char *what) {
+        const double now = omp_get_wtime();
+        if (verbose) fprintf(stderr, "pars3 plan:   locality: %-20s %.3f s\n", what, now - t_prev);
+        t_prev = now;
+    };
     try {
         // 1. the split's entries as one lower CSR (outer entries of a row
         //    precede its middle ones; both ascending: split.py:116-141)
@@ -89,6 +98,7 @@ int locality_order(const pars3_split_view *s, LocalityOrder &out) {
         std::vector<int32_t> ix(2 * m);
         int rc = pars3_pattern_from_lower(n, rp.data(), col.data(), ip.data(), ix.data());
         if (rc) return rc;
+        lap("symmetric pattern");
         // 3. cycle support of every directed edge; keep[e] is symmetric
         std::vector<uint8_t> keep(2 * m, 1);
         std::vector<uint8_t> hub(n, 0);
@@ -132,6 +142,7 @@ int locality_order(const pars3_split_view *s, LocalityOrder &out) {
                 }
             }
         }
+        lap("cycle support");
         // 4. the filtered pattern (still ascending) and its RCM order
         std::vector<int64_t> fp(n + 1, 0);
 #pragma omp parallel for schedule(static)
@@ -152,8 +163,10 @@ int locality_order(const pars3_split_view *s, LocalityOrder &out) {
         std::vector<int32_t>().swap(ix);
         std::vector<uint8_t>().swap(keep);
         std::vector<int64_t> fw(n);
+        lap("filtered pattern");
         rc = pars3_rcm_order(n, fp.data(), fx.data(), fw.data(), 0);
         if (rc) return rc;
+        lap("RCM");
         // 5. P A P^T (skew relabel: an entry that lands above the diagonal is
         //    stored mirrored with its sign flipped)
         out.forward.assign(fw.begin(), fw.end());

@@ -261,9 +261,17 @@ __global__ void __launch_bounds__(kT) k_draft(Split S, Opts o, int64_t nranges, 
             __syncthreads();
             if (tid == 0) {
                 int act = s_action;
-                if (check_terms && s_best + s_maxsegs > o.terms_cap) {  // (the host would halve or chunk)
-                    act = 3;
-                    s_why |= 2;
+                if (act == 0 && check_terms && s_best + s_maxsegs > o.terms_cap) {
+                    // the busiest slot would take more terms than the accumulator
+                    // carries: halve the range (down to terms_min_rows rows), so the
+                    // plan keeps the two-word accumulator; a single row is cut into
+                    // chunks by the host builder
+                    if (b - a > max(1, o.terms_min_rows)) {
+                        act = 2;
+                    } else if (b - a == 1) {
+                        act = 3;
+                        s_why |= 2;
+                    }
                 }
                 int nw = s_ns;
                 bool as_list = false, one_window = false;
