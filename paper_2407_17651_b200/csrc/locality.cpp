@@ -36,6 +36,8 @@ extern "C" int pars3_pattern_from_lower(int64_t n, const int64_t *row_ptr, const
                                         int64_t *indptr, int32_t *indices);
 extern "C" int pars3_rcm_order(int64_t n, const int64_t *indptr, const int32_t *indices,
                                int64_t *forward, int nthreads);
+extern "C" int pars3_rcm_order_via_device(int64_t n, const int64_t *indptr, const int32_t *indices,
+                                          int64_t *forward);
 extern "C" int pars3_permute_lower(int64_t n, const int64_t *row_ptr, const int32_t *col_ind,
                                    const double *off_diags, const double *diags,
                                    const int64_t *forward, int64_t *out_row_ptr,
@@ -160,13 +162,29 @@ int locality_order(const pars3_split_view *s, LocalityOrder &out) {
                 if (keep[e]) fx[o++] = ix[e];
         }
         out.dropped = 2 * m - fp[n];
+        if (verbose)
+            fprintf(stderr, "pars3 plan:   locality: dropped %.1f %% of the directed edges\n",
+                    100.0 * (double)out.dropped / (double)(2 * m));
+        // most edges close no short cycle: there is no band to recover; or the
+        // filter dropped next to nothing (R-MAT: its hubs keep every edge): the
+        // order would be the RCM the caller's labels already are
+        if ((10 * out.dropped > 6 * 2 * m || 1000 * out.dropped < 2 * m) && !getenv("PARS3_LOCALITY_ALWAYS")) {
+            out.forward.clear();
+            return PARS3_OK;
+        }
         std::vector<int32_t>().swap(ix);
         std::vector<uint8_t>().swap(keep);
         std::vector<int64_t> fw(n);
         lap("filtered pattern");
-        rc = pars3_rcm_order(n, fp.data(), fx.data(), fw.data(), 0);
-        if (rc) return rc;
-        lap("RCM");
+        // (on the device when there is one: the same labels, csrc/rcm.cu)
+        const char *hr = getenv("PARS3_LOCALITY_HOST_RCM");
+        const bool on_device = !(hr && hr[0] == '1') &&
+                               pars3_rcm_order_via_device(n, fp.data(), fx.data(), fw.data()) == PARS3_OK;
+        if (!on_device) {
+            rc = pars3_rcm_order(n, fp.data(), fx.data(), fw.data(), 0);
+            if (rc) return rc;
+        }
+        lap(on_device ? "RCM (device)" : "RCM (host)");
         // 5. P A P^T (skew relabel: an entry that lands above the diagonal is
         //    stored mirrored with its sign flipped)
         out.forward.assign(fw.begin(), fw.end());
@@ -190,7 +208,7 @@ extern "C" int pars3_locality_order(const pars3_split_view *s, int64_t *forward,
     pars3::LocalityOrder lo;
     const int rc = pars3::locality_order(s, lo);
     if (rc) return rc;
-    for (int64_t i = 0; i < s->n; i++) forward[i] = lo.forward[i];
+    for (int64_t i = 0; i < s->n; i++) forward[i] = lo.forward.empty() ? i : lo.forward[i];  // (empty: no order)
     if (dropped) *dropped = lo.dropped;
     return PARS3_OK;
 }

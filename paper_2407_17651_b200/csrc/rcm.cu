@@ -495,3 +495,33 @@ extern "C" int pars3_rcm_order_lower_device(int64_t n, const int64_t *row_ptr, c
     RC(cudaGetLastError());
     return rcm_device(n, ip.p, ix.p, forward, st);
 }
+
+// Internal (locality.cpp): RCM of a symmetric pattern held in HOST arrays,
+// computed on the current device when there is one: upload, rcm_device, the
+// labels back.  Returns non-zero (without setting an error the caller must
+// report) when no device is usable; the caller then runs the host RCM, which
+// gives the same labels bit for bit.
+extern "C" int pars3_rcm_order_via_device(int64_t n, const int64_t *indptr, const int32_t *indices,
+                                          int64_t *forward) {
+    int dev = 0;
+    if (n <= 0 || n >= INT32_MAX || cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return PARS3_ERR_CUDA;
+    }
+    const int64_t m2 = indptr[n];
+    DevBuf<int64_t> ip, fw;
+    DevBuf<int32_t> ix;
+    if (ip.alloc(n + 1) != cudaSuccess || ix.alloc(m2) != cudaSuccess || fw.alloc(n) != cudaSuccess ||
+        cudaMemcpy(ip.p, indptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+        (m2 > 0 && cudaMemcpy(ix.p, indices, sizeof(int32_t) * m2, cudaMemcpyHostToDevice) != cudaSuccess)) {
+        cudaGetLastError();
+        return PARS3_ERR_CUDA;
+    }
+    const int rc = rcm_device(n, ip.p, ix.p, fw.p, nullptr);
+    if (rc) return rc;
+    if (cudaMemcpy(forward, fw.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        return PARS3_ERR_CUDA;
+    }
+    return PARS3_OK;
+}

@@ -389,6 +389,7 @@ int build_tile_plan(int64_t n, const int64_t *mid_ptr, const int32_t *mid_col,
             std::vector<int32_t> scratch;
 #pragma omp for schedule(dynamic, 4)
             for (int64_t q = 0; q < nranges; q++) {
+                if (o.sample_stride > 1 && q % o.sample_stride != 0) continue;
                 int32_t a = (int32_t)(q * o.tile_rows);
                 int32_t b = (int32_t)std::min<int64_t>(n, (q + 1) * (int64_t)o.tile_rows);
                 draft_range(R, a, b, o, drafts[q], scratch);

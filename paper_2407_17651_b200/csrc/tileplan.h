@@ -35,6 +35,8 @@ struct PlanOptions {
                                 // terms_cap - 2 segments)
     int32_t terms_min_rows = 256;
     bool skip_empty = false;    // rows without entries get no own slot (no diagonal term)
+    int32_t sample_stride = 1;  // > 1: only every sample_stride-th row range is built (a partial
+                                // plan, for structure estimates only: pars3_plan_create)
     std::vector<int32_t> cuts;  // ascending local indices no window may straddle (peer mode)
 };
 

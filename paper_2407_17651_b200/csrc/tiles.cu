@@ -1680,26 +1680,60 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
         ~DpGuard() { d.release(); }
     } dpg;
     pars3::DevicePlan &dp = dpg.d;
-    int rc = build(s, o, words, hp, &dp);
-    if (rc) return rc;
-    lap(dp.rec ? "tile plan (device)" : "tile plan (host)");
-    int64_t local = local_of(hp);
+    const bool may_permute =
+        !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_NO_LOCALITY | PARS3_PLAN_DIRECT)) && s->n > 1;
+    const int64_t m_total = (s->mid_ptr ? s->mid_ptr[s->n] : 0) + s->outer_count;
+    // A sample of the row ranges first (every k-th range, host builder): when
+    // it shows an unstructured matrix -- mostly list tiles with few entries
+    // per slot -- the locality order is tried before paying for the full
+    // plan in the caller's labels, which is then built only if that fails.
+    int rc = PARS3_OK;
+    bool deferred = false, direct_sample = false;
+    int64_t local = 0;
+    {
+        const int64_t nranges = (s->n + o0.tile_rows - 1) / std::max(1, o0.tile_rows);
+        const char *ns_env = getenv("PARS3_NO_SAMPLE");  // A/B knob
+        if (may_permute && nranges >= 512 && m_total > 0 && !(ns_env && ns_env[0] == '1')) {
+            PlanOptions os = o0;
+            os.terms_cap = words0 == 2 ? kTerms2 : 0;
+            os.local_slots = std::min(want_local, words0 == 3 ? kLocalFixed : kLocalExact);
+            os.sink = (uint16_t)(words0 == 3 ? Layout<3>::kSink : Layout<0>::kSink);
+            os.sample_stride = (int32_t)(nranges / 64);
+            HostPlan hs;
+            rc = pars3::build_tile_plan(s->n, s->mid_ptr, s->mid_col, s->mid_val, s->outer_count, s->outer_row,
+                                        s->outer_col, s->outer_val, os, hs);
+            if (rc) return rc;
+            const int64_t ls = local_of(hs);
+            if (hs.nnz > 0 && 2ll * hs.list_tiles > (int64_t)hs.tiles.size() && 4 * ls > hs.nnz) {
+                deferred = true;
+                local = (int64_t)((double)ls * (double)m_total / (double)hs.nnz);  // the full plan's, estimated
+                direct_sample = 10 * ls >= 9 * hs.nnz;  // about one entry per slot: the row-major form
+            }
+            lap("structure sample");
+        }
+    }
+    if (!deferred) {
+        rc = build(s, o, words, hp, &dp);
+        if (rc) return rc;
+        lap(dp.rec ? "tile plan (device)" : "tile plan (host)");
+        local = local_of(hp);
+    }
     // internal locality order (locality.cpp): tried when most tiles are
     // unstructured list tiles whose slots hold few entries each, kept when
     // it cuts the shared-memory slots (= x gathers + y reductions) by 30 %
     LocalityOrder lo;
     FarSplit fs;  // the near part's arrays (the tiles' split) and the far part, when used
     bool far_used = false;
-    const bool may_permute =
-        !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_NO_LOCALITY | PARS3_PLAN_DIRECT)) && s->n > 1;
-    const bool unstructured = 2ll * hp.list_tiles > (int64_t)hp.tiles.size() && 4 * local > hp.nnz;
-    if (may_permute && (unstructured || (flags & PARS3_PLAN_LOCALITY)) && hp.nnz > 0) {
+    const bool unstructured =
+        deferred || (2ll * hp.list_tiles > (int64_t)hp.tiles.size() && 4 * local > hp.nnz);
+    if (may_permute && (unstructured || (flags & PARS3_PLAN_LOCALITY)) && m_total > 0) {
         rc = pars3::locality_order(s, lo);
         if (rc) return rc;
         lap("locality order");
+        const bool no_order = lo.forward.empty();  // (no local structure to recover: locality.cpp)
         // first with the long-range entries taken out (window-mode tiles + the far part) ...
         const char *nf_env = getenv("PARS3_NO_FAR");  // A/B knob
-        if (!(nf_env && nf_env[0] == '1')) {
+        if (!no_order && !(nf_env && nf_env[0] == '1')) {
             const int32_t T = std::min(want_local, words0 == 3 ? kLocalFixed : kLocalExact) - 640;
             if (T >= 256 && split_far(lo, s->n, T, fs)) {
                 pars3_split_view vn{s->n, s->beta, lo.diag.data(), fs.nptr.data(), fs.ncol.data(),
@@ -1729,7 +1763,7 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
             }
         }
         // ... else every entry in the tiles
-        if (!far_used) {
+        if (!far_used && !no_order) {
             fs = FarSplit();
             pars3_split_view v{s->n, s->beta, lo.diag.data(), lo.row_ptr.data(), lo.col.data(),
                                lo.val.data(), 0, nullptr, nullptr, nullptr};
@@ -1750,6 +1784,19 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
                 lo = LocalityOrder();
             }
         }
+    }
+    // (PARS3_PLAN_LOCALITY forces the attempt on small matrices in tests: such
+    // a plan was never deferred)
+    direct_sample = direct_sample && deferred && lo.forward.empty() &&
+                    !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_SKIP_EMPTY | PARS3_PLAN_NO_DIRECT));
+    if (direct_sample) {
+        hp = HostPlan();  // the row-major form needs no tiles
+        hp.nnz = m_total;
+    } else if (deferred && lo.forward.empty()) {  // no order was kept: the plan in the caller's labels after all
+        rc = build(s, o, words, hp, &dp);
+        if (rc) return rc;
+        lap(dp.rec ? "tile plan (device)" : "tile plan (host)");
+        local = local_of(hp);
     }
     // the split the tiles were built from (the caller's, or P A P^T)
     pars3_split_view used = *s;
@@ -1773,7 +1820,7 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
     const bool direct =
         lo.forward.empty() && hp.nnz > 0 &&
         !(flags & (PARS3_PLAN_CUT_BLOCKS | PARS3_PLAN_SKIP_EMPTY | PARS3_PLAN_NO_DIRECT)) &&
-        ((flags & PARS3_PLAN_DIRECT) || few_tiles ||
+        ((flags & PARS3_PLAN_DIRECT) || few_tiles || direct_sample ||
          (2ll * hp.list_tiles > (int64_t)hp.tiles.size() && 10 * local >= 9 * hp.nnz));
     pars3::FullCsr F;
     if (direct) {  // the full CSR of A (fullcsr.cpp)
