@@ -2094,7 +2094,7 @@ static int launch_red(pars3_plan *pl, const double *x, double *y, bool acc, cuda
             P, x, y, nullptr, nullptr, 0);
     LAUNCH_CHECK();
     if (pl->nfar > 0) {
-        k_far_red<<<std::min(148 * 8, (pl->nfar + 255) / 256), 256, 0, st>>>(P, x, y);
+        k_far_red<<<std::min(148 * 64, (pl->nfar + 255) / 256), 256, 0, st>>>(P, x, y);
         LAUNCH_CHECK();
     }
     mark(pl, st);
@@ -2129,7 +2129,7 @@ static int launch_grid(pars3_plan *pl, const double *x, double *y, const double 
         k_tiles<3, false, true><<<pl->grid, kThreads, pl->smem, st>>>(P, x, y, w, dot, ds);
     LAUNCH_CHECK();
     if (pl->nfar > 0) {
-        k_far_grid<<<std::min(148 * 8, (pl->nfar + 255) / 256), 256, 0, st>>>(P, x);
+        k_far_grid<<<std::min(148 * 64, (pl->nfar + 255) / 256), 256, 0, st>>>(P, x);
         LAUNCH_CHECK();
     }
     mark(pl, st);
