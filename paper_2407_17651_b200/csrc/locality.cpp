@@ -61,6 +61,15 @@ int locality_order(const pars3_split_view *s, LocalityOrder &out) {
         if (verbose) fprintf(stderr, "pars3 plan:   locality: %-20s %.3f s\n", what, now - t_prev);
         t_prev = now;
     };
+    {
+        const char *lh = getenv("PARS3_LOCALITY_HOST");
+        if (!(lh && lh[0] == '1')) {
+            bool done = false;
+            const int rc = locality_order_device(s, out, done);
+            if (rc) return rc;
+            if (done) return PARS3_OK;
+        }
+    }
     try {
         // 1. the split's entries as one lower CSR (outer entries of a row
         //    precede its middle ones; both ascending: split.py:116-141)

@@ -16,7 +16,12 @@ struct LocalityOrder {
     int64_t dropped = 0;           // directed edges the filter removed before the layering
 };
 
-// RCM of the split's graph after dropping the edges no short cycle supports.
+// RCM of the split's graph after dropping the edges no short cycle supports
+// (forward empty: the filter found no band to recover).  Runs on the current
+// device when there is one (locality_gpu.cu: the same result bit for bit;
+// PARS3_LOCALITY_HOST=1 keeps it on the host).
 int locality_order(const pars3_split_view *s, LocalityOrder &out);
+// done = false: not run (no device): the caller runs the host version
+int locality_order_device(const pars3_split_view *s, LocalityOrder &out, bool &done);
 
 }  // namespace pars3
