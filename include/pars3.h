@@ -214,6 +214,12 @@ int pars3_plan_status(pars3_plan *plan, int32_t *flags, void *stream);
 int pars3_full_csr_host(const pars3_split_view *split, int64_t *sizes, int32_t *col, double *val,
                         int32_t *lane_row, uint32_t *lane_flags, int32_t *span_row, int32_t *span_w0,
                         int32_t *span_w1);
+/* The same arrays from the device builder (csrc/fullcsr_gpu.cu), with its
+ * lane-interleaved storage undone: equal to pars3_full_csr_host's entry for
+ * entry (tests). */
+int pars3_full_csr_device(const pars3_split_view *split, int64_t *sizes, int32_t *col, double *val,
+                          int32_t *lane_row, uint32_t *lane_flags, int32_t *span_row, int32_t *span_w0,
+                          int32_t *span_w1);
 
 /* Phase times (CUDA events on `stream`) averaged over `reps` products y = A x
  * (with <y, y> when with_dot): ms[0] the main kernel (tile kernel or full

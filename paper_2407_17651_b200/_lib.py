@@ -83,6 +83,7 @@ _SIGS = {
     "pars3_tile_plan_arrays": (ctypes.c_int, [_vp, _vp, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_locality_order": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, ctypes.POINTER(_c_i64)]),
     "pars3_full_csr_host": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pars3_full_csr_device": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_plan_profile": (ctypes.c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _vp, _vp]),
     "pars3_plan_product": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _c_i32, _vp]),
     "pars3_plan_status": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i32), _vp]),

@@ -48,6 +48,7 @@
 
 #include "common.h"
 #include "fullcsr.h"
+#include "fullcsr_gpu.h"
 
 // PARS3_CHECKS builds (make checked -> libpars3_checked.so, selected with
 // PARS3_LIB): device-side bounds checks on every shared slot, row and column
@@ -1823,9 +1824,22 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
         ((flags & PARS3_PLAN_DIRECT) || few_tiles || direct_sample ||
          (2ll * hp.list_tiles > (int64_t)hp.tiles.size() && 10 * local >= 9 * hp.nnz));
     pars3::FullCsr F;
-    if (direct) {  // the full CSR of A (fullcsr.cpp)
-        rc = pars3::build_full_csr(s, F);
-        if (rc) return rc;
+    struct DfGuard {
+        pars3::DeviceFullCsr d;
+        ~DfGuard() { d.release(); }
+    } dfg;
+    pars3::DeviceFullCsr &DF = dfg.d;
+    if (direct) {  // the full CSR of A: on the device (fullcsr_gpu.cu), else on the host (fullcsr.cpp)
+        bool on_device = false;
+        if (may_device) {
+            rc = pars3::build_full_csr_device(s, DF, on_device);
+            if (rc) return rc;
+        }
+        if (!on_device) {
+            rc = pars3::build_full_csr(s, F);
+            if (rc) return rc;
+        }
+        lap(on_device ? "full CSR (device)" : "full CSR (host)");
         const int64_t m_entries = hp.nnz;
         hp = HostPlan();  // no tiles are uploaded
         hp.nnz = m_entries;
@@ -1905,7 +1919,24 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
         }                                                                                     \
         pl->bytes += (int64_t)_b;                                                             \
     } while (0)
-    if (direct) {
+    if (direct && DF.col) {  // built on the device (already lane-interleaved): the plan takes the arrays
+        pl->direct = 1;
+        pl->built_on_device = 1;
+        pl->ne = DF.ne;
+        pl->nwarps = DF.nep / pars3::kCsrWarp;
+        pl->nspan = DF.nspan;
+        pl->ccol = DF.col;
+        pl->cval = DF.val;
+        pl->clrow = DF.lane_row;
+        pl->clflags = DF.lane_flags;
+        pl->span_row = DF.span_row;
+        pl->span_w0 = DF.span_w0;
+        pl->span_w1 = DF.span_w1;
+        pl->bytes += (int64_t)(12 * DF.nep + 8 * (DF.nep / pars3::kCsrLane) + 12 * (int64_t)DF.nspan);
+        DF = pars3::DeviceFullCsr();
+        ZALLOC(whead, std::max<int64_t>(1, pl->nwarps));
+        ZALLOC(wtail, std::max<int64_t>(1, pl->nwarps));
+    } else if (direct) {
         {  // lane-interleaved storage within each warp of 512 entries (k_csr)
             const int64_t nw = (int64_t)F.col.size() / pars3::kCsrWarp;
             std::vector<int32_t> c2(F.col.size());

@@ -163,3 +163,41 @@ def test_resident_split_plan(lib_built, oracle):
     assert np.array_equal(y, y2)
     ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x)
     assert oracle.rel_err(y, ref) <= 1e-12
+
+
+def _full_csr(s, device):
+    L = _lib.load()
+    v, keep = _view(s)
+    fn = L.pars3_full_csr_device if device else L.pars3_full_csr_host
+    sizes = np.zeros(4, dtype=np.int64)
+    _lib.check(fn(ctypes.byref(v), _lib.ptr(sizes), None, None, None, None, None, None, None))
+    nep, ne, nl, nsp = (int(t) for t in sizes)
+    out = dict(col=np.zeros(nep, np.int32), val=np.zeros(nep, np.float64), lane_row=np.zeros(nl, np.int32),
+               lane_flags=np.zeros(nl, np.uint32), span_row=np.zeros(max(nsp, 1), np.int32),
+               span_w0=np.zeros(max(nsp, 1), np.int32), span_w1=np.zeros(max(nsp, 1), np.int32))
+    _lib.check(fn(ctypes.byref(v), _lib.ptr(sizes), *(_lib.ptr(out[k]) for k in
+                                                      ("col", "val", "lane_row", "lane_flags", "span_row",
+                                                       "span_w0", "span_w1"))))
+    for k in ("span_row", "span_w0", "span_w1"):
+        out[k] = out[k][:nsp]
+    out["sizes"] = sizes
+    return out
+
+
+@pytest.mark.parametrize("name", ["rmat", "band_far", "stencil27", "grid5", "varying_diag"])
+def test_device_full_csr(name, lib_built):
+    """The row-major plan built on the device (csrc/fullcsr_gpu.cu) equals the
+    host builder's (csrc/fullcsr.cpp) entry for entry: hub rows spanning many
+    warps, empty rows (diagonal only), padding, constant and varying diagonals."""
+    g = {"rmat": lambda: G.rmat(13, 16, seed_struct=7, seed_perm=8, seed_val=9),
+         "band_far": lambda: G.random_band(30001, 700, 9, 0.03, seed_struct=1, seed_perm=2, seed_val=3),
+         "stencil27": lambda: G.stencil27(12, seed_val=6, alpha=0.5),
+         "grid5": lambda: G.grid5(30, seed_perm=7, seed_val=8),
+         "varying_diag": lambda: G.rmat(11, 8, seed_struct=1, seed_perm=2, seed_val=3)}[name]()
+    m, s = _split(g)
+    if name == "varying_diag":
+        s = P.BandSplit(s.n, s.beta, np.linspace(-1.0, 2.0, s.n), s.mid_ptr, s.mid_col, s.mid_val, s.outer_row,
+                        s.outer_col, s.outer_val)
+    host, dev = _full_csr(s, False), _full_csr(s, True)
+    for k in host:
+        assert np.array_equal(host[k], dev[k]), (name, k)
