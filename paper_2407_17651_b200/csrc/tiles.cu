@@ -1071,11 +1071,12 @@ __global__ void __launch_bounds__(512) k_xmax(int32_t n, const double *__restric
 }
 
 // <a, b>: 16-byte loads, four in flight per thread; each block writes its
-// share to part[blockIdx.x] and k_sum_parts adds the shares in block order
-// (a fixed reduction order: the dot is bitwise repeatable)
+// share to part[blockIdx.x]; the block that finishes last adds the shares in
+// block order (a fixed reduction order: the dot is bitwise repeatable) into
+// *out.  part[kDotGrid] holds the arrival counter (zero between calls).
 constexpr int kDotGrid = 148 * 4;
 __global__ void __launch_bounds__(512) k_dot(int32_t n, const double *__restrict__ a,
-                                             const double *__restrict__ b, double *part) {
+                                             const double *__restrict__ b, double *part, double *out) {
     double s = 0.0;
     const int64_t n2 = n / 2;
     const double2 *a2 = reinterpret_cast<const double2 *>(a);
@@ -1101,10 +1102,33 @@ __global__ void __launch_bounds__(512) k_dot(int32_t n, const double *__restrict
     __shared__ double ws[16];
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
     __syncthreads();
+    __shared__ int s_last;
     if (threadIdx.x < 32) {
         s = threadIdx.x < 16 ? ws[threadIdx.x] : 0.0;
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (threadIdx.x == 0) part[blockIdx.x] = s;
+        if (threadIdx.x == 0) {
+            part[blockIdx.x] = s;
+            __threadfence();
+            unsigned int *arrived = reinterpret_cast<unsigned int *>(part + kDotGrid);
+            s_last = atomicAdd(arrived, 1u) == gridDim.x - 1;
+            if (s_last) {
+                *arrived = 0u;
+                __threadfence();
+            }
+        }
+    }
+    __syncthreads();
+    if (!s_last) return;
+    double d = 0.0;  // shares in block order per thread, then a fixed tree
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) d += __ldcg(part + i);
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = d;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        d = threadIdx.x < 16 ? ws[threadIdx.x] : 0.0;
+        for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (threadIdx.x == 0) *out = d;
     }
 }
 
@@ -1998,7 +2022,7 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
         ZALLOC(ys, pl->n);
     }
     ZALLOC(gs, 1);
-    ZALLOC(part, kDotGrid);
+    ZALLOC(part, kDotGrid + 1);  // (+ k_dot's arrival counter)
     static_assert(kConvGrid >= kDotGrid, "blk_dot / blk_max hold k_conv's shares");
     {
         GState g0{};
@@ -2211,9 +2235,7 @@ static int launch_dot(int64_t n, const double *a, const double *b, double *part,
         return PARS3_OK;
     }
     if (((uintptr_t)a | (uintptr_t)b) & 15) PARS3_FAIL(PARS3_ERR_ARG, "vectors must be 16-byte aligned");
-    k_dot<<<kDotGrid, 512, 0, st>>>((int32_t)n, a, b, part);
-    LAUNCH_CHECK();
-    k_sum_parts<<<1, kThreads, 0, st>>>(kDotGrid, part, out);
+    k_dot<<<kDotGrid, 512, 0, st>>>((int32_t)n, a, b, part, out);
     LAUNCH_CHECK();
     return PARS3_OK;
 }
@@ -2368,7 +2390,8 @@ extern "C" int pars3_dot(int64_t n, const double *a, const double *b, double *ou
     cudaStream_t st = (cudaStream_t)stream;
     // stream-ordered scratch for the per-block shares (pool allocation)
     double *part = nullptr;
-    CUDA_TRY(cudaMallocAsync((void **)&part, sizeof(double) * kDotGrid, st));
+    CUDA_TRY(cudaMallocAsync((void **)&part, sizeof(double) * (kDotGrid + 1), st));
+    CUDA_TRY(cudaMemsetAsync(part + kDotGrid, 0, sizeof(double), st));  // the arrival counter
     const int rc = launch_dot(n, a, b, part, out, st);
     CUDA_TRY(cudaFreeAsync(part, st));
     return rc;
@@ -2394,13 +2417,13 @@ extern "C" int pars3_plan_kernel_count(const pars3_plan *pl, int32_t with_dot, i
     const bool grid = pl->grid_ok && pl->peers.nranks == 0 && pl->ntiles > 0;
     int c = 0;
     if (pl->direct) {
-        c = (pl->n > 0 ? 1 : 0) + (pl->nspan > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 2 : 0);
+        c = (pl->n > 0 ? 1 : 0) + (pl->nspan > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 1 : 0);
     } else if (pl->perm) {
         c = 2 + (pl->ntiles > 0 ? (grid ? 3 : 1) : 0) + (pl->nfar > 0 ? 1 : 0);
     } else if (grid) {
         c = 3;  // k_tiles, k_conv, k_finish (exits at once unless the product was flagged)
     } else {
-        c = (pl->ntiles > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 2 : 0);
+        c = (pl->ntiles > 0 ? 1 : 0) + (pl->nfar > 0 ? 1 : 0) + (with_dot && pl->n > 0 ? 1 : 0);
     }
     *count = c;
     return PARS3_OK;

@@ -430,9 +430,9 @@ def test_locality_order(flags, oracle):
         _, dot2 = op.matvec_dot(xd, xd)
         assert abs(float(dot2.item()) - float(x @ yh)) <= 1e-12 * float(np.abs(x) @ np.abs(yh))
         # grid form: tiles + k_conv + k_finish; + perm in/out with a locality
-        # order; row-major form: full CSR + span fix-up + dot (two kernels)
+        # order; row-major form: full CSR + span fix-up + dot (one kernel)
         # (one more for the far part: the long-range entries kept out of the tiles)
-        expect = 5 + (1 if st["far_entries"] else 0) if st["locality_order"] else 4 if st["direct"] else 3
+        expect = 5 + (1 if st["far_entries"] else 0) if st["locality_order"] else 3 if st["direct"] else 3
         assert op.kernel_count(True) == expect, st
         if flags == 8 and g.name.startswith("random_band"):
             # the far part (k_far_grid / k_far_red): window-mode tiles for the band,
@@ -489,4 +489,4 @@ def test_direct_mode(flags, oracle):
             assert abs(float(dot.item()) - float(yh @ yh)) <= 1e-12 * float(yh @ yh)
             assert op.status() & 1 == 0  # no product redone
             if st["direct"]:
-                assert op.kernel_count(True) == 4
+                assert op.kernel_count(True) == 3  # k_csr, the span fix-up, the dot
