@@ -883,7 +883,11 @@ int build_tile_plan_device(int64_t n, const int64_t *mid_ptr, const int32_t *mid
     RC(flags.alloc(8));
     RC(cudaMemset(flags.p, 0, 8 * sizeof(int32_t)));
     const size_t smem = 2 * (kBitmapBits / 8) + kCounters * 2;
-    RC(cudaFuncSetAttribute((const void *)k_draft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (cudaFuncSetAttribute((const void *)k_draft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {  // (a device without 192 KB of shared memory per CTA: the host builder)
+        cudaGetLastError();
+        return PARS3_OK;
+    }
     k_draft<<<(unsigned)nranges, kT, smem>>>(S, oo, nranges, draft.p, ntl.p, flags.p);
     RC(cudaGetLastError());
     int32_t hf[8] = {0};
