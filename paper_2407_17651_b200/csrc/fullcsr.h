@@ -11,7 +11,10 @@
 
 namespace pars3 {
 
-constexpr int kCsrLane = 16;                  // entries per lane
+#ifndef PARS3_CSR_LANE  // tuning builds
+#define PARS3_CSR_LANE 16
+#endif
+constexpr int kCsrLane = PARS3_CSR_LANE;      // entries per lane (<= 16: the row-start mask has 32 bits)
 constexpr int kCsrWarp = 32 * kCsrLane;       // entries per warp
 
 struct FullCsr {

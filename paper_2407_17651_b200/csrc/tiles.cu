@@ -1215,7 +1215,10 @@ __global__ void __launch_bounds__(512) k_perm_out(int32_t n, const int32_t *__re
 // partials in warp order.  No atomics: every y element is written once, the
 // sum order is fixed by the plan (bitwise repeatable), and the arithmetic
 // is plain fp64 (IEEE semantics for non-finite inputs).
-__global__ void __launch_bounds__(256, 2) k_csr(int32_t nrows, int64_t ne, int64_t nwarps,
+#ifndef PARS3_CSR_MINB  // tuning builds
+#define PARS3_CSR_MINB 2
+#endif
+__global__ void __launch_bounds__(256, PARS3_CSR_MINB) k_csr(int32_t nrows, int64_t ne, int64_t nwarps,
                                                 const int32_t *__restrict__ col,
                                                 const double *__restrict__ val,
                                                 const int32_t *__restrict__ lane_row,
@@ -1345,7 +1348,7 @@ struct pars3_plan {
     int32_t p = 1;
     int32_t ntiles = 0, nslices = 0, lmax = 0;
     int64_t nnz = 0, slots = 0, nwins = 0;
-    int grid = 0, grid_redo = 0, conv_grid = 0;
+    int grid = 0, grid_redo = 0, conv_grid = 0, csr_grid = 148 * 2;
     size_t smem = 0;
     TileMeta *tiles = nullptr;
     Window *wins = nullptr;
@@ -2080,6 +2083,12 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
     if (max_ctas > 0 && pl->grid > max_ctas) pl->grid = max_ctas;
     if (pl->grid > pl->ntiles) pl->grid = pl->ntiles > 0 ? pl->ntiles : 1;
     pl->grid_redo = std::min(pl->grid, per_sm_redo * sms);
+    {  // k_csr: one resident wave of CTAs
+        int per_sm_csr = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_csr, k_csr, 256, 0) != cudaSuccess || per_sm_csr < 1)
+            per_sm_csr = 1;
+        pl->csr_grid = per_sm_csr * sms;
+    }
     {  // k_conv: one resident wave (measured: 1 184 CTAs in four waves 58 us, one wave of 296 52 us on c5)
         int per_sm_conv = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_conv, k_conv, kConvThreads, 0) != cudaSuccess ||
@@ -2210,7 +2219,7 @@ static int launch_direct(pars3_plan *pl, const double *x, double *y, bool acc, c
         if (!pl->yacc_tmp) CUDA_TRY(cudaMalloc((void **)&pl->yacc_tmp, sizeof(double) * (size_t)pl->n));
         out = pl->yacc_tmp;
     }
-    const int grid = (int)std::min<int64_t>(148 * 2, (pl->nwarps + 7) / 8);
+    const int grid = (int)std::min<int64_t>(pl->csr_grid, (pl->nwarps + 7) / 8);
     k_csr<<<grid, 256, 0, st>>>((int32_t)pl->n, pl->ne, pl->nwarps, pl->ccol, pl->cval, pl->clrow, pl->clflags, x, out,
                                 pl->whead, pl->wtail);
     LAUNCH_CHECK();
