@@ -181,6 +181,16 @@ int pars3_plan_spmv(pars3_plan *plan, const double *x, double *y, void *stream);
 int pars3_plan_product(pars3_plan *plan, const double *x, double *y, const double *w, double *dot,
                        int32_t flags, void *stream);
 
+/* The product fused with the vector update that follows it in a Krylov step:
+ * out = A x + (*a) p + (*b) q and, when dot != NULL, *dot = <out, out>
+ * (MRS: u = A v - alpha v + gamma w and ||u||^2).  a and b are DEVICE
+ * scalars: the recurrence needs no host round trip.  Grid-form plans apply
+ * the update in the finish pass (no separate y is written and read back);
+ * other forms run the product and one more pass.  flags:
+ * PARS3_PRODUCT_STRICT.  out must not alias x, p or q. */
+int pars3_plan_product_axpy(pars3_plan *plan, const double *x, double *out, const double *p, const double *a,
+                            const double *q, const double *b, double *dot, int32_t flags, void *stream);
+
 /* y += A x through a plan (y is NOT zeroed): several plans over the same
  * index space (e.g. a rank's interior and boundary rows, DistributedPars3)
  * accumulate into one y. */

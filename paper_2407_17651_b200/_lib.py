@@ -86,6 +86,7 @@ _SIGS = {
     "pars3_full_csr_device": (ctypes.c_int, [ctypes.POINTER(SplitView), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_plan_profile": (ctypes.c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _vp, _vp]),
     "pars3_plan_product": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _c_i32, _vp]),
+    "pars3_plan_product_axpy": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i32, _vp]),
     "pars3_plan_status": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i32), _vp]),
     "pars3_plan_kernel_count": (ctypes.c_int, [_vp, _c_i32, ctypes.POINTER(_c_i32)]),
     "pars3_plan_destroy": (ctypes.c_int, [_vp]),

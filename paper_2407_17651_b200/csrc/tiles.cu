@@ -198,6 +198,10 @@ struct DevPlan {
     const int32_t *far_row, *far_col;
     const double *far_val;
     int32_t nfar;
+    // fused epilogue of pars3_plan_product_axpy: out = A x + (*ep_a) p + (*ep_b) q
+    // (device scalars, so an iteration's recurrence needs no host round trip);
+    // null ep_a: none
+    const double *ep_p, *ep_q, *ep_a, *ep_b;
 };
 
 
@@ -860,7 +864,9 @@ __global__ void __launch_bounds__(kConvThreads, PARS3_CONV_MINB) k_conv(DevPlan 
     const int64_t stride = (int64_t)gridDim.x * kConvThreads;
     const int64_t i0 = blockIdx.x * (int64_t)kConvThreads + threadIdx.x;
     double d = 0.0, mx = 0.0;
-    if ((((uintptr_t)y | (uintptr_t)w) & 15) == 0) {  // pairs: 16-byte accesses
+    const bool ep = P.ep_a != nullptr;
+    const double ea = ep ? *P.ep_a : 0.0, eb = ep ? *P.ep_b : 0.0;
+    if ((((uintptr_t)y | (uintptr_t)w | (uintptr_t)P.ep_p | (uintptr_t)P.ep_q) & 15) == 0) {  // pairs: 16-byte accesses
         const int64_t n2 = n / 2;
         longlong2 *a2 = reinterpret_cast<longlong2 *>(P.yacc);
         double2 *y2 = reinterpret_cast<double2 *>(y);
@@ -876,32 +882,40 @@ __global__ void __launch_bounds__(kConvThreads, PARS3_CONV_MINB) k_conv(DevPlan 
                 const int64_t j = i + u * stride;
                 if (j < n2) {
                     if (!P.yclear) __stcs(a2 + j, make_longlong2(0, 0));
-                    const double2 v = make_double2((double)Y[u].x * gunit, (double)Y[u].y * gunit);
+                    double2 v = make_double2((double)Y[u].x * gunit, (double)Y[u].y * gunit);
+                    mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));  // (of A x: the grid's accuracy check)
+                    if (ep) {
+                        const double2 pp = __ldcs(reinterpret_cast<const double2 *>(P.ep_p) + j);
+                        const double2 qq = __ldcs(reinterpret_cast<const double2 *>(P.ep_q) + j);
+                        v.x = fma(eb, qq.x, fma(ea, pp.x, v.x));
+                        v.y = fma(eb, qq.y, fma(ea, pp.y, v.y));
+                    }
                     __stcs(y2 + j, v);
                     if (dot) {
                         const double2 q = self ? v : __ldcs(w2 + j);
                         d = fma(v.y, q.y, fma(v.x, q.x, d));
                     }
-                    mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
                 }
             }
         }
         if ((n & 1) && i0 == 0) {
             const long long Y = P.yacc[n - 1];
             if (!P.yclear) P.yacc[n - 1] = 0;
-            const double v = (double)Y * gunit;
+            double v = (double)Y * gunit;
+            mx = fmax(mx, fabs(v));
+            if (ep) v = fma(eb, P.ep_q[n - 1], fma(ea, P.ep_p[n - 1], v));
             y[n - 1] = v;
             if (dot) d = fma(v, self ? v : w[n - 1], d);
-            mx = fmax(mx, fabs(v));
         }
     } else {
         for (int64_t i = i0; i < n; i += stride) {
             const long long Y = P.yacc[i];
             if (!P.yclear) P.yacc[i] = 0;
-            const double v = (double)Y * gunit;
+            double v = (double)Y * gunit;
+            mx = fmax(mx, fabs(v));
+            if (ep) v = fma(eb, P.ep_q[i], fma(ea, P.ep_p[i], v));
             y[i] = v;
             if (dot) d = fma(v, self ? v : w[i], d);
-            mx = fmax(mx, fabs(v));
         }
     }
     // fixed-tree CTA sums (cta_sum's shape with this CTA size)
@@ -999,11 +1013,17 @@ k_finish(DevPlan P, const double *__restrict__ x, double *__restrict__ y, const 
         atomicAdd(y + c, -v * x[i]);
     }
     grid_sync(g);
-    if (dot) {  // per-CTA shares in blk_dot (>= kDotGrid entries), summed in CTA order
+    if (dot || P.ep_a) {  // the fused epilogue; per-CTA shares in blk_dot, summed in CTA order
+        const bool ep = P.ep_a != nullptr;
+        const double ea = ep ? *P.ep_a : 0.0, eb = ep ? *P.ep_b : 0.0;
         double d = 0.0;
         for (int64_t i = i0; i < n; i += stride) {
-            const double v = __ldcg(y + i);
-            d = fma(v, dot_self ? v : w[i], d);
+            double v = __ldcg(y + i);
+            if (ep) {
+                v = fma(eb, P.ep_q[i], fma(ea, P.ep_p[i], v));
+                y[i] = v;
+            }
+            if (dot) d = fma(v, dot_self ? v : w[i], d);
         }
         d = cta_sum(d, s_red);
         if (threadIdx.x == 0) P.blk_dot[blockIdx.x] = d;
@@ -1367,6 +1387,7 @@ struct pars3_plan {
     double *blk_dot = nullptr, *blk_max = nullptr, *part = nullptr;
     long long *yacc = nullptr, *yacc2 = nullptr;  // (yacc2: the second accumulator, PARS3 two-buffer form)
     int32_t acc_turn = 0;
+    const double *ep_p = nullptr, *ep_q = nullptr, *ep_a = nullptr, *ep_b = nullptr;  // this call's fused epilogue
     int32_t seen_fp64_tiles = 0, seen_redone = 0;  // pars3_plan_status: counters at its last call
     cudaEvent_t *prof = nullptr;  // pars3_plan_profile: events at the product's phase boundaries
     int prof_k = 0;
@@ -2130,6 +2151,10 @@ static DevPlan dev_plan(const pars3_plan *pl) {
     P.far_col = pl->far_col;
     P.far_val = pl->far_val;
     P.nfar = pl->nfar;
+    P.ep_p = pl->ep_p;
+    P.ep_q = pl->ep_q;
+    P.ep_a = pl->ep_a;
+    P.ep_b = pl->ep_b;
     return P;
 }
 
@@ -2339,6 +2364,47 @@ extern "C" int pars3_plan_product(pars3_plan *pl, const double *x, double *y, co
     if ((flags & PARS3_PRODUCT_ACC) && dot) PARS3_FAIL(PARS3_ERR_ARG, "y += A x has no fused dot");
     return plan_product(pl, x, y, (flags & PARS3_PRODUCT_ACC) != 0, w, dot, (cudaStream_t)stream,
                         (flags & PARS3_PRODUCT_STRICT) != 0);
+}
+
+// out[i] = out[i] + (*a) p[i] + (*b) q[i]  (the unfused form of pars3_plan_product_axpy's epilogue)
+__global__ void __launch_bounds__(512) k_axpy2(int32_t n, double *out, const double *__restrict__ p,
+                                               const double *a, const double *__restrict__ q, const double *b) {
+    const double ea = *a, eb = *b;
+    const int32_t stride = gridDim.x * blockDim.x;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = fma(eb, q[i], fma(ea, p[i], out[i]));
+}
+
+// out = A x + (*a) p + (*b) q and, when dot is given, *dot = <out, out>: the
+// product fused with the vector update that follows it in a Krylov step (MRS:
+// u = A v - alpha v + gamma w).  a, b are DEVICE scalars, so the recurrence
+// needs no host round trip.  Grid-form plans apply the update in the finish
+// pass (no separate y is written or read back); the other forms run the
+// product and one more pass.  out must not alias x, p or q.
+extern "C" int pars3_plan_product_axpy(pars3_plan *pl, const double *x, double *out, const double *p,
+                                       const double *a, const double *q, const double *b, double *dot,
+                                       int32_t flags, void *stream) {
+    if (!pl || !a || !b || (pl->n > 0 && (!x || !out || !p || !q))) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
+    if (flags & PARS3_PRODUCT_ACC) PARS3_FAIL(PARS3_ERR_ARG, "pars3_plan_product_axpy overwrites out");
+    if (pl->n > 0 && (out == p || out == q)) PARS3_FAIL(PARS3_ERR_ARG, "out must not alias p or q");
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool strict = (flags & PARS3_PRODUCT_STRICT) != 0;
+    const bool fused = pl->grid_ok && pl->peers.nranks == 0 && pl->ntiles > 0 && !pl->perm && !pl->direct;
+    if (fused) {
+        pl->ep_p = p;
+        pl->ep_q = q;
+        pl->ep_a = a;
+        pl->ep_b = b;
+        const int rc = plan_product(pl, x, out, false, dot ? out : nullptr, dot, st, strict);
+        pl->ep_p = pl->ep_q = pl->ep_a = pl->ep_b = nullptr;
+        return rc;
+    }
+    int rc = plan_product(pl, x, out, false, nullptr, nullptr, st, strict);
+    if (rc || pl->n == 0) return rc;
+    k_axpy2<<<kDotGrid, 512, 0, st>>>((int32_t)pl->n, out, p, a, q, b);
+    LAUNCH_CHECK();
+    if (dot) rc = launch_dot(pl->n, out, out, pl->part, dot, st);
+    return rc;
 }
 
 extern "C" int pars3_plan_spmv(pars3_plan *pl, const double *x, double *y, void *stream) {

@@ -113,6 +113,19 @@ class Pars3Operator:
                                               _lib.stream_ptr(stream)), "pars3_plan_product")
         return y, dot
 
+    def matvec_axpy(self, x, out, p, a, q, b, dot=None, stream=None, strict=False):
+        """out = A x + a p + b q and, with ``dot`` (a device scalar tensor),
+        dot = <out, out>: the product fused with the vector update that
+        follows it in a Krylov step (pars3_plan_product_axpy).  ``a`` and ``b``
+        are one-element CUDA tensors (device scalars, e.g. views of a solver's
+        state), so the recurrence needs no host round trip.  ``out`` must not
+        alias x, p or q."""
+        _lib.check(self._L.pars3_plan_product_axpy(
+            self._handle, _lib.ptr(x), _lib.ptr(out), _lib.ptr(p), _lib.ptr(a), _lib.ptr(q), _lib.ptr(b),
+            _lib.ptr(dot) if dot is not None else None, _lib.PRODUCT_STRICT if strict else 0,
+            _lib.stream_ptr(stream)), "pars3_plan_product_axpy")
+        return out
+
     # -- host-resident vectors: pipelined copies --------------------------
     def matvec_host(self, x, out=None, non_blocking=False, strict=True):
         """y = A x for a HOST float64 tensor x (pinned for overlap), result in

@@ -78,28 +78,41 @@ def mrs_solve(op, b, alpha: float, tol: float = 1e-10, maxiter: int = 100, strea
     state[5:7] = beta_t.expand(2)
     state[14] = float(tol)
     state[15] = float(alpha)
+    state[18] = -float(alpha)  # (the fused product's coefficient of v)
     resid[0:1] = beta_t
     x = torch.zeros(n, dtype=t, device=dev)
     v = b / torch.where(beta_t > 0, beta_t, torch.ones_like(beta_t))  # v_j
     w = torch.zeros(n, dtype=t, device=dev)   # v_{j-1}, then u
     dm1 = torch.zeros(n, dtype=t, device=dev)  # d_{j-1}
     dm2 = torch.zeros(n, dtype=t, device=dev)  # d_{j-2}, then d_j
-    y = torch.empty(n, dtype=t, device=dev)
+    y = torch.empty(n, dtype=t, device=dev)   # A v_j; with the fused product: the free buffer u lands in
+    # the product fused with the Lanczos update (pars3_plan_product_axpy): u = A v - alpha v +
+    # gamma w and ||u||^2 in the product's finish pass, no y written and read back
+    fused = group is None and hasattr(op, "matvec_axpy")
     res = MrsResult(x=x, iterations=0)
     if float(beta_t.item()) == 0.0:
         res.residuals, res.converged = [0.0], True
         return res
     j = 0
     for j in range(1, maxiter + 1):
-        op.matvec(v, y, stream=stream, strict=True)  # each product a pure function of v
-        _lib.check(L.pars3_mrs_lanczos_dev(n, _lib.ptr(y), _lib.ptr(v), _lib.ptr(w), _lib.ptr(state),
-                                           _lib.ptr(part), st), "mrs_lanczos")
-        allreduce(state[7:8])  # the step's inner product, summed over ranks
+        if fused:
+            # u (in y's buffer) = A v - alpha v + gamma w, state[7] = ||u||^2; strict: a pure function of v
+            op.matvec_axpy(v, y, v, state[18:19], w, state[0:1], dot=state[7:8], stream=stream, strict=True)
+            u = y
+        else:
+            op.matvec(v, y, stream=stream, strict=True)  # each product a pure function of v
+            _lib.check(L.pars3_mrs_lanczos_dev(n, _lib.ptr(y), _lib.ptr(v), _lib.ptr(w), _lib.ptr(state),
+                                               _lib.ptr(part), st), "mrs_lanczos")
+            allreduce(state[7:8])  # the step's inner product, summed over ranks
+            u = w
         _lib.check(L.pars3_mrs_rotate_dev(_lib.ptr(state), _lib.ptr(resid), j, st), "mrs_rotate")
-        _lib.check(L.pars3_mrs_update_dev(n, _lib.ptr(w), _lib.ptr(v), _lib.ptr(dm2), _lib.ptr(dm1),
+        _lib.check(L.pars3_mrs_update_dev(n, _lib.ptr(u), _lib.ptr(v), _lib.ptr(dm2), _lib.ptr(dm1),
                                           _lib.ptr(x), _lib.ptr(state), st), "mrs_update")
-        # rotate the buffers: v_{j+1} <- w, v_j -> w's slot; d_j <- dm2
-        v, w = w, v
+        # rotate the buffers: v_{j+1} <- u, v_j -> w's slot (fused: old w becomes the free buffer); d_j <- dm2
+        if fused:
+            v, w, y = y, v, w
+        else:
+            v, w = w, v
         dm1, dm2 = dm2, dm1
         if check_every and j % check_every == 0 and float(state[16].item()) != 0.0:
             break

@@ -490,3 +490,45 @@ def test_direct_mode(flags, oracle):
             assert op.status() & 1 == 0  # no product redone
             if st["direct"]:
                 assert op.kernel_count(True) == 3  # k_csr, the span fix-up, the dot
+
+
+def test_product_axpy(oracle):
+    """pars3_plan_product_axpy: out = A x + a p + b q and <out, out> (device
+    scalars a, b), fused into the finish pass of grid-form plans, one more
+    pass for the other forms; the fp64 redo applies it as well."""
+    import torch
+    from paper_2407_17651_b200 import generators as G
+    from paper_2407_17651_b200.device import operator_for_sss
+    cases = [(G.stencil27(24, seed_val=6, alpha=0.5), (0, 0, 0, -1, 0, 64, 0)),      # grid form (fused)
+             (G.stencil27(20, seed_val=7, alpha=0.5), (0, 0, 0, -1, 0, 32, 0)),      # row-major form
+             (G.random_band(30000, 600, 12, 0.01, seed_struct=1, seed_perm=2, seed_val=3), (0, 0, 0, -1, 0, 8, 0))]
+    rng = np.random.default_rng(4)
+    for g, opts in cases:
+        m0 = P.SssMatrix._trusted(g.n, g.row_ptr, g.col_ind, g.off_diags, g.diags)
+        m = P.permute_sss(m0, P.rcm_order(P.pattern_from_sss(m0)))
+        op = operator_for_sss(m, options=opts)
+        x, p, q = (rng.uniform(-1, 1, m.n) for _ in range(3))
+        coef = torch.tensor([-0.5, 1.75], dtype=torch.float64, device="cuda")
+        y_ref = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, x)
+        want = y_ref - 0.5 * p + 1.75 * q
+        xd, pd, qd = (torch.from_numpy(a).cuda() for a in (x, p, q))
+        out = torch.empty_like(xd)
+        dot = torch.zeros(1, dtype=torch.float64, device="cuda")
+        for strict in (False, True):
+            op.matvec_axpy(xd, out, pd, coef[0:1], qd, coef[1:2], dot=dot, strict=strict)
+            got = out.cpu().numpy()
+            assert rel_err(got, want) <= TOL, (g.name, op.stats())
+            assert abs(float(dot.item()) - float(got @ got)) <= 1e-12 * float(got @ got)
+        op.matvec_axpy(xd, out, pd, coef[0:1], qd, coef[1:2])      # without the dot
+        assert rel_err(out.cpu().numpy(), want) <= TOL
+        # the redo (a non-finite x): IEEE result, the update applied once
+        xi = x.copy()
+        xi[m.n // 2] = np.inf
+        ref_i = oracle.spmv_serial(m.row_ptr, m.col_ind, m.off_diags, m.diags, xi) - 0.5 * p + 1.75 * q
+        op.matvec_axpy(torch.from_numpy(xi).cuda(), out, pd, coef[0:1], qd, coef[1:2], dot=dot)
+        got_i = out.cpu().numpy()
+        fin = np.isfinite(ref_i)
+        assert np.array_equal(np.isfinite(got_i), fin)
+        assert rel_err(got_i[fin], ref_i[fin]) <= TOL
+        with pytest.raises(ValueError):
+            op.matvec_axpy(xd, out, out, coef[0:1], qd, coef[1:2])   # out aliases p
