@@ -178,6 +178,11 @@ int pars3_plan_spmv(pars3_plan *plan, const double *x, double *y, void *stream);
  * over this x instead (a pure function of x; one extra read of x). */
 #define PARS3_PRODUCT_ACC 1
 #define PARS3_PRODUCT_STRICT 2
+/* With STRICT in pars3_plan_product_axpy: the bound of this x is already in
+ * the plan's device slot (pars3_plan_xbound_slot), written by the kernel that
+ * produced x (pars3_mrs_update_dev2), so the product skips its pass over x.
+ * A wrong bound is caught on the device and the product redone. */
+#define PARS3_PRODUCT_XBOUND 4
 int pars3_plan_product(pars3_plan *plan, const double *x, double *y, const double *w, double *dot,
                        int32_t flags, void *stream);
 
@@ -190,6 +195,11 @@ int pars3_plan_product(pars3_plan *plan, const double *x, double *y, const doubl
  * PARS3_PRODUCT_STRICT.  out must not alias x, p or q. */
 int pars3_plan_product_axpy(pars3_plan *plan, const double *x, double *out, const double *p, const double *a,
                             const double *q, const double *b, double *dot, int32_t flags, void *stream);
+
+/* The device word for PARS3_PRODUCT_XBOUND: 0 = none, else e + 1 + 2048 where
+ * |x_i| < 2^e for every finite x_i (e = max(biased exponent, 1) - 1022),
+ * combined with atomicMax.  *slot = NULL when the plan cannot use it. */
+int pars3_plan_xbound_slot(pars3_plan *plan, int32_t **slot);
 
 /* y += A x through a plan (y is NOT zeroed): several plans over the same
  * index space (e.g. a rank's interior and boundary rows, DistributedPars3)
@@ -304,6 +314,10 @@ int pars3_mrs_lanczos_dev(int64_t n, const double *y, const double *v, double *w
 int pars3_mrs_rotate_dev(double *state, double *resid, int32_t j, void *stream);
 int pars3_mrs_update_dev(int64_t n, double *u, const double *v, double *dm2, const double *dm1, double *x,
                          const double *state, void *stream);
+/* The same, also leaving the bound of the new u (the next product's x) in
+ * xe_slot (pars3_plan_xbound_slot; may be NULL). */
+int pars3_mrs_update_dev2(int64_t n, double *u, const double *v, double *dm2, const double *dm1, double *x,
+                          const double *state, int32_t *xe_slot, void *stream);
 
 /* --------------------------------------------- host-native preprocessing */
 

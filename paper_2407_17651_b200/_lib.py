@@ -54,7 +54,8 @@ PLAN_DIRECT = 32       # direct mode (no shared staging) forced (pars3.h)
 PLAN_NO_DIRECT = 64    # never direct mode
 PLAN_HOST_BUILD = 128  # tile plan by the host builder (never csrc/tileplan_gpu.cu)
 PRODUCT_ACC = 1        # pars3_plan_product: y += A x
-PRODUCT_STRICT = 2     # the grid scale from this x (a pure function of x)
+PRODUCT_STRICT = 2
+PRODUCT_XBOUND = 4    # with STRICT: x's bound is already in the plan's slot (pars3_plan_xbound_slot)     # the grid scale from this x (a pure function of x)
 
 
 # name -> (restype, argtypes)
@@ -87,6 +88,7 @@ _SIGS = {
     "pars3_plan_profile": (ctypes.c_int, [_vp, _vp, _vp, _c_i32, _c_i32, _vp, _vp]),
     "pars3_plan_product": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _c_i32, _vp]),
     "pars3_plan_product_axpy": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i32, _vp]),
+    "pars3_plan_xbound_slot": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     "pars3_plan_status": (ctypes.c_int, [_vp, ctypes.POINTER(_c_i32), _vp]),
     "pars3_plan_kernel_count": (ctypes.c_int, [_vp, _c_i32, ctypes.POINTER(_c_i32)]),
     "pars3_plan_destroy": (ctypes.c_int, [_vp]),
@@ -97,6 +99,7 @@ _SIGS = {
     "pars3_mrs_lanczos_dev": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_mrs_rotate_dev": (ctypes.c_int, [_vp, _vp, _c_i32, _vp]),
     "pars3_mrs_update_dev": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pars3_mrs_update_dev2": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pars3_mrs_update": (ctypes.c_int, [_c_i64, _vp, ctypes.c_double, _vp, _vp, _vp,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_double, _vp, _vp]),

@@ -161,16 +161,36 @@ __global__ void __launch_bounds__(32) k_rotate_dev(double *st, double *resid, in
     }
 }
 
+// (xe_slot: the bound of the new u for the next product, in k_xmax's
+// encoding, tiles.cu: max(biased exponent, 1) - 1022 + 1 + 2048 over the
+// finite values)
 __global__ void __launch_bounds__(kBlock) k_update_dev(int64_t n, double *u, const double *__restrict__ v,
                                                        double *dm2, const double *__restrict__ dm1, double *x,
-                                                       const double *st) {
+                                                       const double *st, int32_t *xe_slot) {
     if (st[kDone] != 0.0) return;
     const double r0 = st[kR0], r1 = st[kR1], inv_r2 = st[kInvR2], tau = st[kTau], inv_g = st[kInvG];
+    int e = -1100;
+    // (four CTAs per SM as before the bound was added: the compiler's deeper
+    // unrolling took 116 registers and ran the pass three times slower)
+#pragma unroll 1
     for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         const double d = (v[i] - r0 * dm2[i] - r1 * dm1[i]) * inv_r2;
         dm2[i] = d;
         x[i] = fma(tau, d, x[i]);
-        u[i] *= inv_g;
+        const double un = u[i] * inv_g;
+        u[i] = un;
+        const int b = (int)((__double_as_longlong(un) >> 52) & 0x7FF);
+        if (b != 2047) e = max(e, max(b, 1) - 1022);
+    }
+    if (xe_slot) {  // one atomic per CTA at most, and only when it would raise the bound
+        __shared__ int s_e;
+        if (threadIdx.x == 0) s_e = -1100;
+        __syncthreads();
+        e = __reduce_max_sync(0xffffffffu, e);
+        if ((threadIdx.x & 31) == 0 && e > -1100) atomicMax(&s_e, e);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_e > -1100 && s_e + 1 + 2048 > *(volatile int32_t *)xe_slot)
+            atomicMax(xe_slot, s_e + 1 + 2048);
     }
 }
 
@@ -205,7 +225,18 @@ extern "C" int pars3_mrs_update_dev(int64_t n, double *u, const double *v, doubl
                                     double *x, const double *state, void *stream) {
     if (n < 0 || !state || (n > 0 && (!u || !v || !dm2 || !dm1 || !x))) PARS3_FAIL(PARS3_ERR_ARG, "bad arguments");
     if (n == 0) return PARS3_OK;
-    k_update_dev<<<grid_for(n), kBlock, 0, (cudaStream_t)stream>>>(n, u, v, dm2, dm1, x, state);
+    k_update_dev<<<grid_for(n), kBlock, 0, (cudaStream_t)stream>>>(n, u, v, dm2, dm1, x, state, nullptr);
+    LAUNCH_CHECK();
+    return PARS3_OK;
+}
+
+extern "C" int pars3_mrs_update_dev2(int64_t n, double *u, const double *v, double *dm2, const double *dm1,
+                                     double *x, const double *state, int32_t *xe_slot, void *stream) {
+    if (n < 0 || !state || (n > 0 && (!u || !v || !dm2 || !dm1 || !x))) PARS3_FAIL(PARS3_ERR_ARG, "bad arguments");
+    if (n == 0) return PARS3_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (xe_slot) CUDA_TRY(cudaMemsetAsync(xe_slot, 0, sizeof(int32_t), st));
+    k_update_dev<<<grid_for(n), kBlock, 0, st>>>(n, u, v, dm2, dm1, x, state, xe_slot);
     LAUNCH_CHECK();
     return PARS3_OK;
 }

@@ -1388,6 +1388,7 @@ struct pars3_plan {
     long long *yacc = nullptr, *yacc2 = nullptr;  // (yacc2: the second accumulator, PARS3 two-buffer form)
     int32_t acc_turn = 0;
     const double *ep_p = nullptr, *ep_q = nullptr, *ep_a = nullptr, *ep_b = nullptr;  // this call's fused epilogue
+    bool xbound_given = false;  // this call: the caller stored x's bound in gs->xe_pre (PARS3_PRODUCT_XBOUND)
     int32_t seen_fp64_tiles = 0, seen_redone = 0;  // pars3_plan_status: counters at its last call
     cudaEvent_t *prof = nullptr;  // pars3_plan_profile: events at the product's phase boundaries
     int prof_k = 0;
@@ -2201,7 +2202,10 @@ static int launch_grid(pars3_plan *pl, const double *x, double *y, const double 
         P.yclear = pl->acc_turn ? pl->yacc : pl->yacc2;
         pl->acc_turn ^= 1;
     }
-    if (strict || !pl->xe_ready) {  // the scale bound from a pass over this x
+    if (strict && pl->xbound_given) {  // the caller's kernel already stored this x's bound
+        pl->xe_ready = 1;
+        P.strict = 1;
+    } else if (strict || !pl->xe_ready) {  // the scale bound from a pass over this x
         CUDA_TRY(cudaMemsetAsync(&pl->gs->xe_pre, 0, sizeof(int32_t), st));
         const int grid = (int)std::min<int64_t>(148 * 4, (pl->n + 511) / 512);
         k_xmax<<<grid, 512, 0, st>>>((int32_t)pl->n, x, pl->gs);
@@ -2391,12 +2395,14 @@ extern "C" int pars3_plan_product_axpy(pars3_plan *pl, const double *x, double *
     const bool strict = (flags & PARS3_PRODUCT_STRICT) != 0;
     const bool fused = pl->grid_ok && pl->peers.nranks == 0 && pl->ntiles > 0 && !pl->perm && !pl->direct;
     if (fused) {
+        pl->xbound_given = strict && (flags & PARS3_PRODUCT_XBOUND) != 0;
         pl->ep_p = p;
         pl->ep_q = q;
         pl->ep_a = a;
         pl->ep_b = b;
         const int rc = plan_product(pl, x, out, false, dot ? out : nullptr, dot, st, strict);
         pl->ep_p = pl->ep_q = pl->ep_a = pl->ep_b = nullptr;
+        pl->xbound_given = false;
         return rc;
     }
     int rc = plan_product(pl, x, out, false, nullptr, nullptr, st, strict);
@@ -2470,6 +2476,18 @@ extern "C" int pars3_dot(int64_t n, const double *a, const double *b, double *ou
     const int rc = launch_dot(n, a, b, part, out, st);
     CUDA_TRY(cudaFreeAsync(part, st));
     return rc;
+}
+
+// The device word a caller's kernel may fill with the bound of the next x
+// (PARS3_PRODUCT_XBOUND): 0 = none, else (e + 1 + 2048) with |x_i| < 2^e for
+// every finite x_i (e = max(biased exponent, 1) - 1022): k_xmax's encoding.
+// *slot = NULL for plans without the grid form or whose x passes through an
+// internal order first.
+extern "C" int pars3_plan_xbound_slot(pars3_plan *pl, int32_t **slot) {
+    if (!pl || !slot) PARS3_FAIL(PARS3_ERR_ARG, "null argument");
+    const bool ok = pl->grid_ok && pl->peers.nranks == 0 && pl->ntiles > 0 && !pl->perm && !pl->direct;
+    *slot = ok ? &pl->gs->xe_pre : nullptr;
+    return PARS3_OK;
 }
 
 extern "C" int pars3_plan_status(pars3_plan *pl, int32_t *flags, void *stream) {

@@ -113,16 +113,25 @@ class Pars3Operator:
                                               _lib.stream_ptr(stream)), "pars3_plan_product")
         return y, dot
 
-    def matvec_axpy(self, x, out, p, a, q, b, dot=None, stream=None, strict=False):
+    def xbound_slot(self):
+        """Device address (int, 0 when the plan has none) of the word a kernel
+        may fill with the bound of the next x (pars3_plan_xbound_slot)."""
+        slot = ctypes.c_void_p()
+        _lib.check(self._L.pars3_plan_xbound_slot(self._handle, ctypes.byref(slot)), "pars3_plan_xbound_slot")
+        return int(slot.value or 0)
+
+    def matvec_axpy(self, x, out, p, a, q, b, dot=None, stream=None, strict=False, xbound=False):
         """out = A x + a p + b q and, with ``dot`` (a device scalar tensor),
         dot = <out, out>: the product fused with the vector update that
         follows it in a Krylov step (pars3_plan_product_axpy).  ``a`` and ``b``
         are one-element CUDA tensors (device scalars, e.g. views of a solver's
         state), so the recurrence needs no host round trip.  ``out`` must not
-        alias x, p or q."""
+        alias x, p or q.  ``xbound`` (with ``strict``): the kernel that produced
+        x left its bound in ``xbound_slot()``, so the product skips its pass over x."""
         _lib.check(self._L.pars3_plan_product_axpy(
             self._handle, _lib.ptr(x), _lib.ptr(out), _lib.ptr(p), _lib.ptr(a), _lib.ptr(q), _lib.ptr(b),
-            _lib.ptr(dot) if dot is not None else None, _lib.PRODUCT_STRICT if strict else 0,
+            _lib.ptr(dot) if dot is not None else None,
+            (_lib.PRODUCT_STRICT if strict else 0) | (_lib.PRODUCT_XBOUND if strict and xbound else 0),
             _lib.stream_ptr(stream)), "pars3_plan_product_axpy")
         return out
 

@@ -89,6 +89,13 @@ def mrs_solve(op, b, alpha: float, tol: float = 1e-10, maxiter: int = 100, strea
     # the product fused with the Lanczos update (pars3_plan_product_axpy): u = A v - alpha v +
     # gamma w and ||u||^2 in the product's finish pass, no y written and read back
     fused = group is None and hasattr(op, "matvec_axpy")
+    # the update pass leaves the bound of v_{j+1} in the plan's slot, so the strict product skips its pass over v
+    slot = op.xbound_slot() if fused and hasattr(op, "xbound_slot") else 0
+    import os
+    if os.environ.get("PARS3_MRS_NO_XBOUND") == "1":  # A/B knob
+        slot = 0
+    if os.environ.get("PARS3_MRS_NO_FUSE") == "1":
+        fused, slot = False, 0
     res = MrsResult(x=x, iterations=0)
     if float(beta_t.item()) == 0.0:
         res.residuals, res.converged = [0.0], True
@@ -97,7 +104,8 @@ def mrs_solve(op, b, alpha: float, tol: float = 1e-10, maxiter: int = 100, strea
     for j in range(1, maxiter + 1):
         if fused:
             # u (in y's buffer) = A v - alpha v + gamma w, state[7] = ||u||^2; strict: a pure function of v
-            op.matvec_axpy(v, y, v, state[18:19], w, state[0:1], dot=state[7:8], stream=stream, strict=True)
+            op.matvec_axpy(v, y, v, state[18:19], w, state[0:1], dot=state[7:8], stream=stream, strict=True,
+                           xbound=bool(slot) and j > 1)
             u = y
         else:
             op.matvec(v, y, stream=stream, strict=True)  # each product a pure function of v
@@ -106,8 +114,8 @@ def mrs_solve(op, b, alpha: float, tol: float = 1e-10, maxiter: int = 100, strea
             allreduce(state[7:8])  # the step's inner product, summed over ranks
             u = w
         _lib.check(L.pars3_mrs_rotate_dev(_lib.ptr(state), _lib.ptr(resid), j, st), "mrs_rotate")
-        _lib.check(L.pars3_mrs_update_dev(n, _lib.ptr(u), _lib.ptr(v), _lib.ptr(dm2), _lib.ptr(dm1),
-                                          _lib.ptr(x), _lib.ptr(state), st), "mrs_update")
+        _lib.check(L.pars3_mrs_update_dev2(n, _lib.ptr(u), _lib.ptr(v), _lib.ptr(dm2), _lib.ptr(dm1),
+                                           _lib.ptr(x), _lib.ptr(state), slot or None, st), "mrs_update")
         # rotate the buffers: v_{j+1} <- u, v_j -> w's slot (fused: old w becomes the free buffer); d_j <- dm2
         if fused:
             v, w, y = y, v, w
