@@ -852,6 +852,8 @@ __device__ __forceinline__ void grid_sync(GState *g) {
 #endif
 constexpr int kConvThreads = 256;
 constexpr int kConvGrid = 148 * 8;  // (the most CTAs; the launch uses one resident wave)
+// (kEp: with pars3_plan_product_axpy's update; the plain instantiation keeps its registers)
+template <bool kEp>
 __global__ void __launch_bounds__(kConvThreads, PARS3_CONV_MINB) k_conv(DevPlan P, double *__restrict__ y, const double *w,
                                                        double *dot, int dot_self, int32_t n) {
     __shared__ double s_red[kConvThreads / 32];
@@ -864,9 +866,9 @@ __global__ void __launch_bounds__(kConvThreads, PARS3_CONV_MINB) k_conv(DevPlan 
     const int64_t stride = (int64_t)gridDim.x * kConvThreads;
     const int64_t i0 = blockIdx.x * (int64_t)kConvThreads + threadIdx.x;
     double d = 0.0, mx = 0.0;
-    const bool ep = P.ep_a != nullptr;
+    constexpr bool ep = kEp;
     const double ea = ep ? *P.ep_a : 0.0, eb = ep ? *P.ep_b : 0.0;
-    if ((((uintptr_t)y | (uintptr_t)w | (uintptr_t)P.ep_p | (uintptr_t)P.ep_q) & 15) == 0) {  // pairs: 16-byte accesses
+    if ((((uintptr_t)y | (uintptr_t)w | (ep ? (uintptr_t)P.ep_p | (uintptr_t)P.ep_q : 0)) & 15) == 0) {  // pairs: 16-byte accesses
         const int64_t n2 = n / 2;
         longlong2 *a2 = reinterpret_cast<longlong2 *>(P.yacc);
         double2 *y2 = reinterpret_cast<double2 *>(y);
@@ -2113,7 +2115,7 @@ extern "C" int pars3_plan_create_resident(const pars3_split_view *s, const pars3
     }
     {  // k_conv: one resident wave (measured: 1 184 CTAs in four waves 58 us, one wave of 296 52 us on c5)
         int per_sm_conv = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_conv, k_conv, kConvThreads, 0) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_conv, k_conv<true>, kConvThreads, 0) != cudaSuccess ||
             per_sm_conv < 1)
             per_sm_conv = 1;
         pl->conv_grid = std::min(kConvGrid, per_sm_conv * sms);
@@ -2227,7 +2229,10 @@ static int launch_grid(pars3_plan *pl, const double *x, double *y, const double 
     }
     mark(pl, st);
     int32_t n32 = (int32_t)pl->n;
-    k_conv<<<pl->conv_grid, kConvThreads, 0, st>>>(P, y, w, dot, ds, n32);
+    if (P.ep_a)
+        k_conv<true><<<pl->conv_grid, kConvThreads, 0, st>>>(P, y, w, dot, ds, n32);
+    else
+        k_conv<false><<<pl->conv_grid, kConvThreads, 0, st>>>(P, y, w, dot, ds, n32);
     LAUNCH_CHECK();
     void *args[] = {(void *)&P, (void *)&x, (void *)&y, (void *)&w, (void *)&dot, (void *)&ds, (void *)&n32};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_finish, dim3(pl->grid_redo), dim3(kThreads), args,
