@@ -119,7 +119,9 @@ int pars3_locality_order(const pars3_split_view *split, int64_t *forward, int64_
  * column windows and uploaded; the host arrays may be freed
  * afterwards.  `p`/`block_start` (host int64[p+1], partition_rows
  * split.py:173-188) record the row-block ownership for the multi-GPU path;
- * a single-GPU plan passes p = 1. */
+ * a single-GPU plan passes p = 1.  A plan carries per-product state (the
+ * accumulator in turn, scale bounds, redo flags): use it from one host thread
+ * at a time, and order its products on one stream. */
 int pars3_plan_create(const pars3_split_view *split, const pars3_plan_options *options,
                       int32_t p, const int64_t *block_start, pars3_plan **out, void *stream);
 
