@@ -574,12 +574,13 @@ def run_gpu(args):
     own_nnz = int(stats["entries"]) + int(stats.get("boundary_entries", 0))
     B_rank = algorithmic_bytes(hi - lo, own_nnz) if world > 1 else B
     achieved = B_rank / (spmv_ms * 1e-3) / 1e9
-    traffic = None
+    traffic = traffic_dom = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath) and world == 1:
         try:
             tj = json.load(open(tpath)).get(args.config)
             traffic = tj.get("bytes") if isinstance(tj, dict) else tj
+            traffic_dom = tj.get("k_tiles") if isinstance(tj, dict) else None
         except Exception:
             traffic = None
     if rank != 0:
@@ -613,7 +614,8 @@ def run_gpu(args):
                                   else "k_tiles"),
                          "ms": phases["main_ms"],
                          "achieved": B_rank / (phases["main_ms"] * 1e-3) / 1e9,
-                         "frac": B_rank / (phases["main_ms"] * 1e-3) / 1e9 / peak}
+                         "frac": B_rank / (phases["main_ms"] * 1e-3) / 1e9 / peak,
+                         "traffic": traffic_dom}
                          if phases and phases.get("main_ms", 0) > 0 else None)},
         "cpu_baseline": cpu,
         "e2e": {"value": B / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
